@@ -1,0 +1,150 @@
+/*
+ * tpf.h — C ABI of the B200-native CommFuse hot path (libtpfuse_b200.so).
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/tpfuse/{collectives,layers}.hpp). Plain
+ * pointers and sizes only; device pointers are raw CUDA device addresses,
+ * streams are cudaStream_t passed as void*. All calls return 0 on success or a
+ * negative TPF_E* code; the message is in tpf_last_error() (thread-local).
+ *
+ * Calls that move data are collective: every rank of a group must make the same
+ * call (same shapes, schedule, granularity) in the same order on one stream.
+ * There is no CPU fallback: without an sm_100 device every data-path call
+ * fails with TPF_E_CUDA.
+ */
+#ifndef TPF_H_
+#define TPF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes. The C++ mirror (include/tpfuse_b200/tpfuse.hpp) maps them to the
+ * reference's exception types. */
+#define TPF_OK 0
+#define TPF_E_INVALID (-1)   /* std::invalid_argument (divisibility, granularity, peers)  */
+#define TPF_E_SHAPE (-2)     /* tpfuse::ShapeError                                       */
+#define TPF_E_LOGIC (-3)     /* std::logic_error (check_schedule)                         */
+#define TPF_E_CUDA (-4)      /* CUDA runtime / launch failure, no device                  */
+#define TPF_E_PEER (-5)      /* peer flag timeout: GroupError(rank, ...)                  */
+#define TPF_E_CAPACITY (-6)  /* symmetric heap too small for this call                    */
+
+/* ScheduleKind, collectives.hpp:19 */
+#define TPF_RING 0
+#define TPF_PAIRWISE 1
+#define TPF_CIRCULAR 2
+
+/* element types */
+#define TPF_BF16 0
+#define TPF_F32 1
+
+/* AG-GEMM epilogue activation (tpsp_mlp_forward's element-wise Activation,
+ * layers.hpp:58; only the exactly-representable ones run fused). */
+#define TPF_ACT_NONE 0
+#define TPF_ACT_SQUARE 1
+
+typedef struct tpf_comm tpf_comm;
+
+int tpf_version(void);
+const char* tpf_last_error(void);
+/* number of SMs on the current device, 0 if no device */
+int tpf_device_sms(void);
+
+/* ---------------------------------------------------------- schedules (host)
+ * Replaces: RingIndices ring_indices_ag/ring_indices_rs(int r, int i, int n)
+ *           (collectives.hpp:51-55, collectives.cpp:47-55).
+ * rs != 0 selects ring_indices_rs. out = {send_peer, recv_peer, compute_slice}. */
+int tpf_ring_indices(int rs, int r, int i, int n, int32_t out[3]);
+
+/* Replaces: Schedule build_schedule(ScheduleKind, int n)  (collectives.hpp:59,
+ * collectives.cpp:57-107). out: n*n*3 int32, [rank][iteration](send, recv,
+ * slice); nothing written for n == 1. Rejections as the reference:
+ * TPF_E_INVALID for n < 1 or odd n with PAIRWISE. */
+int tpf_schedule_build(int kind, int n, int32_t* out);
+
+/* Replaces: void check_schedule(const Schedule&) (collectives.hpp:64,
+ * collectives.cpp:180-235). TPF_E_LOGIC on a violated invariant. */
+int tpf_schedule_check(int kind, int n, const int32_t* table);
+
+/* -------------------------------------------------- communicator (RankEndpoint)
+ * Replaces: RankEndpoint / RankGroup / spawn_group (fabric.hpp:114-226).
+ * One process per GPU: each rank creates its communicator with a symmetric
+ * heap of sym_bytes (device memory exported through CUDA IPC), exports its
+ * handle, the caller exchanges the world's handles out of band (e.g. a
+ * torch.distributed all_gather of the bytes), and opens them. */
+#define TPF_IPC_HANDLE_BYTES 64
+int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out);
+int tpf_comm_ipc_handle(tpf_comm* c, void* handle_out /* TPF_IPC_HANDLE_BYTES */);
+int tpf_comm_open_peers(tpf_comm* c, const void* handles /* world * TPF_IPC_HANDLE_BYTES */);
+
+/* Single-GPU group: all `world` ranks are hosted by this process and every
+ * fused call runs all ranks in ONE persistent launch (ranks own disjoint SM
+ * sets; peer buffers are local). Used to prove the fused P2P protocol on one
+ * GPU. Tensor arguments are then rank-stacked: x[world][...], w[world][...],
+ * out[world][...]. */
+int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm** out);
+
+int tpf_comm_destroy(tpf_comm* c);
+int tpf_comm_rank(const tpf_comm* c);
+int tpf_comm_world(const tpf_comm* c);
+/* Synchronise `stream` and check the device error record of every call since
+ * the last check. TPF_E_PEER names the failing rank/step via tpf_last_error(). */
+int tpf_comm_sync(tpf_comm* c, void* stream);
+/* Test hook (fault injection, fabric_test.cpp:44-58 analogue): shrink the
+ * peer-wait timeout (ns). 0 restores the default. */
+int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns);
+
+/* -------------------------------------------------------------- fused ops
+ * AG-GEMM. Replaces:
+ *   Tensor column_parallel_forward(RankEndpoint&, const Tensor& x,
+ *                                  const ShardedLinear& w, int m = 1)
+ *       (layers.hpp:68-69, layers.cpp:120-127), i.e.
+ *   Tensor fuse_all_gather(RankEndpoint&, const Tensor& x, f = matmul(., W_col[r]), m)
+ *       (collectives.hpp:79-80, collectives.cpp:237-279).
+ *   x   : bf16 (B, S/T, K) row-major — this rank's sequence slice
+ *   w   : bf16 (K, N_local) row-major — this rank's column shard
+ *   out : (B, S, N_local) row-major, out_dtype (TPF_BF16 | TPF_F32)
+ * Ring schedule (ring_indices_ag), granularity m >= 1, S/T divisible by m. */
+int tpf_ag_gemm(tpf_comm* c, const void* x, const void* w, void* out, int64_t B, int64_t S,
+                int64_t K, int64_t N_local, int m, int act, int out_dtype, void* stream);
+
+/* GEMM-RS. Replaces:
+ *   Tensor row_parallel_forward(RankEndpoint&, const Tensor& x, const ShardedLinear& w,
+ *                               const Schedule&, int m = 1)
+ *       (layers.hpp:74-76, layers.cpp:129-138), i.e.
+ *   Tensor fuse_reduce_scatter(RankEndpoint&, const Tensor& x, f = matmul(., W_row[r]),
+ *                              const Schedule&, int m)  (collectives.hpp:87-89,
+ *       collectives.cpp:362-405).
+ *   x   : bf16 (B, S, K_local) row-major — this rank's feature shard
+ *   w   : bf16 (K_local, N) row-major — this rank's row shard
+ *   out : (B, S/T, N) row-major, out_dtype
+ * kind: TPF_RING | TPF_PAIRWISE | TPF_CIRCULAR (reduction order exactly the
+ * reference's); m > 1 only with TPF_RING; S divisible by T*m.
+ * wire_dtype: dtype of the partial sums crossing NVLink (TPF_F32 for parity,
+ * TPF_BF16 halves the bytes; rounds the running sum once per hop). */
+int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B, int64_t S,
+                int64_t K_local, int64_t N, int kind, int m, int wire_dtype, int out_dtype,
+                void* stream);
+
+/* T == 1 degenerate case of both ops (collectives.cpp:242,379): out = a * b.
+ *   a: bf16 (M, K), b: bf16 (K, N), out: (M, N) out_dtype. No communicator. */
+int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
+             int out_dtype, void* stream);
+
+/* Element-wise SwiGLU between the two fused ops of the Llama TP-SP MLP block
+ * (tpsp_mlp_forward, layers.cpp:140-147, with the gate||up column shard):
+ *   gu : bf16 (rows, 2*F) = [gate | up];  out: bf16 (rows, F) = silu(gate) * up */
+int tpf_swiglu(const void* gu, void* out, int64_t rows, int64_t F, void* stream);
+
+/* Bytes of symmetric heap a call needs (per rank), for sizing tpf_comm_create. */
+int64_t tpf_sym_bytes_ag(int world, int64_t B, int64_t S, int64_t K, int64_t N_local, int m);
+int64_t tpf_sym_bytes_rs(int world, int64_t B, int64_t S, int64_t K_local, int64_t N, int m,
+                         int wire_dtype);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPF_H_ */

@@ -1,0 +1,255 @@
+"""B200-native CommFuse hot path (arXiv 2604.24013): fused AG-GEMM / GEMM-RS.
+
+Python host mirror of the reference's operator API for this path
+(/root/reference/proj/include/tpfuse/{collectives,layers}.hpp) over the C ABI
+in include/tpf.h (libtpfuse_b200.so, built in-tree). torch is used only for
+device memory, streams and torch.distributed plumbing.
+
+There is no CPU or PyTorch fallback: if the shared library is missing, import
+fails; if no sm_100 device is present, every data-path call raises TpfCudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtpfuse_b200.so")
+
+RING, PAIRWISE, CIRCULAR = 0, 1, 2
+KIND_NAMES = {RING: "ring", PAIRWISE: "pairwise", CIRCULAR: "circular-slices"}
+BF16, F32 = 0, 1
+ACT_NONE, ACT_SQUARE = 0, 1
+IPC_HANDLE_BYTES = 64
+
+# include/tpf.h error codes -> reference exception types (SURVEY §8(b) Errors)
+E_INVALID, E_SHAPE, E_LOGIC, E_CUDA, E_PEER, E_CAPACITY = -1, -2, -3, -4, -5, -6
+
+
+class ShapeError(ValueError):
+    """tpfuse::ShapeError (a std::invalid_argument)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (check_schedule)."""
+
+
+class GroupError(RuntimeError):
+    """tpfuse::GroupError: a rank failed (here: peer flag wait timed out)."""
+
+
+class TpfCudaError(RuntimeError):
+    """CUDA failure or no sm_100 device."""
+
+
+class CapacityError(RuntimeError):
+    """Symmetric heap too small for the call."""
+
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not built: run `make -C {_HERE}` (or __graft_entry__.build()). "
+        "There is no fallback path.")
+
+_lib = C.CDLL(LIB_PATH)
+_vp, _i64, _i32p = C.c_void_p, C.c_int64, C.POINTER(C.c_int32)
+_lib.tpf_last_error.restype = C.c_char_p
+_lib.tpf_ring_indices.argtypes = [C.c_int] * 4 + [_i32p]
+_lib.tpf_schedule_build.argtypes = [C.c_int, C.c_int, _i32p]
+_lib.tpf_schedule_check.argtypes = [C.c_int, C.c_int, _i32p]
+_lib.tpf_comm_create.argtypes = [C.c_int, C.c_int, C.c_size_t, C.POINTER(_vp)]
+_lib.tpf_comm_create_local_group.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
+_lib.tpf_comm_ipc_handle.argtypes = [_vp, _vp]
+_lib.tpf_comm_open_peers.argtypes = [_vp, _vp]
+_lib.tpf_comm_destroy.argtypes = [_vp]
+_lib.tpf_comm_sync.argtypes = [_vp, _vp]
+_lib.tpf_comm_set_timeout_ns.argtypes = [_vp, _i64]
+_lib.tpf_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 3 + [_vp]
+_lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + [_vp]
+_lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
+_lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
+_lib.tpf_sym_bytes_ag.argtypes = [C.c_int] + [_i64] * 4 + [C.c_int]
+_lib.tpf_sym_bytes_ag.restype = _i64
+_lib.tpf_sym_bytes_rs.argtypes = [C.c_int] + [_i64] * 4 + [C.c_int, C.c_int]
+_lib.tpf_sym_bytes_rs.restype = _i64
+
+EXPORTED_SYMBOLS = (
+    "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
+    "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
+    "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
+    "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
+)
+
+
+def lib() -> C.CDLL:
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = _lib.tpf_last_error().decode()
+    exc = {E_INVALID: ValueError, E_SHAPE: ShapeError, E_LOGIC: LogicError, E_CUDA: TpfCudaError,
+           E_PEER: GroupError, E_CAPACITY: CapacityError}.get(rc, RuntimeError)
+    raise exc(msg)
+
+
+# ------------------------------------------------------------------ schedules
+def ring_indices_ag(r: int, i: int, n: int):
+    """RingIndices ring_indices_ag(r, i, n) (collectives.cpp:47-50)."""
+    out = (C.c_int32 * 3)()
+    _check(_lib.tpf_ring_indices(0, r, i, n, out))
+    return tuple(out)
+
+
+def ring_indices_rs(r: int, i: int, n: int):
+    """RingIndices ring_indices_rs(r, i, n) (collectives.cpp:52-55)."""
+    out = (C.c_int32 * 3)()
+    _check(_lib.tpf_ring_indices(1, r, i, n, out))
+    return tuple(out)
+
+
+def build_schedule(kind: int, n: int):
+    """Schedule build_schedule(kind, n) -> steps[rank][iteration] = (send, recv, slice)."""
+    buf = (C.c_int32 * max(1, n * n * 3))()
+    _check(_lib.tpf_schedule_build(kind, n, buf))
+    if n == 1:
+        return [[]]
+    return [[tuple(buf[(r * n + i) * 3:(r * n + i) * 3 + 3]) for i in range(n)] for r in range(n)]
+
+
+def check_schedule(kind: int, steps) -> None:
+    """void check_schedule(const Schedule&): raises LogicError on violation."""
+    n = len(steps)
+    flat = [v for row in steps for st in row for v in st]
+    buf = (C.c_int32 * max(1, len(flat)))(*flat)
+    _check(_lib.tpf_schedule_check(kind, n, buf))
+
+
+# --------------------------------------------------------------- communicator
+def _stream_ptr(stream) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Communicator:
+    """RankEndpoint analogue (fabric.hpp:114-147) over a CUDA-IPC symmetric heap.
+
+    * ``Communicator.local_group(world, ...)`` — all ranks hosted on the current
+      GPU, every fused call runs the whole group in one persistent launch.
+    * ``Communicator.from_process_group(pg, ...)`` — one process per GPU; IPC
+      handles exchanged with torch.distributed (plumbing only).
+    """
+
+    def __init__(self, handle: int, rank: int, world: int, local_group: bool):
+        self._h = C.c_void_p(handle)
+        self.rank, self.world, self.is_local_group = rank, world, local_group
+
+    @classmethod
+    def local_group(cls, world: int, sym_bytes_per_rank: int) -> "Communicator":
+        h = C.c_void_p()
+        _check(_lib.tpf_comm_create_local_group(world, sym_bytes_per_rank, C.byref(h)))
+        return cls(h.value, 0, world, True)
+
+    @classmethod
+    def create(cls, rank: int, world: int, sym_bytes: int) -> "Communicator":
+        h = C.c_void_p()
+        _check(_lib.tpf_comm_create(rank, world, sym_bytes, C.byref(h)))
+        return cls(h.value, rank, world, False)
+
+    def ipc_handle(self) -> bytes:
+        buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+        _check(_lib.tpf_comm_ipc_handle(self._h, buf))
+        return buf.raw
+
+    def open_peers(self, handles: Sequence[bytes]) -> None:
+        blob = b"".join(handles)
+        assert len(blob) == IPC_HANDLE_BYTES * self.world
+        _check(_lib.tpf_comm_open_peers(self._h, C.c_char_p(blob)))
+
+    @classmethod
+    def from_process_group(cls, sym_bytes: int, group=None) -> "Communicator":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        comm = cls.create(rank, world, sym_bytes)
+        if world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, comm.ipc_handle(), group=group)
+            comm.open_peers(handles)
+            dist.barrier(group)
+        return comm
+
+    def set_timeout_ms(self, ms: float) -> None:
+        _check(_lib.tpf_comm_set_timeout_ns(self._h, int(ms * 1e6)))
+
+    def sync(self, stream=None) -> None:
+        """Synchronise the stream and raise GroupError if a peer wait timed out."""
+        _check(_lib.tpf_comm_sync(self._h, _stream_ptr(stream)))
+
+    def close(self) -> None:
+        if self._h:
+            _lib.tpf_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ fused ops
+    def ag_gemm(self, x, w, out, m: int = 1, act: int = ACT_NONE, stream=None) -> None:
+        """column_parallel_forward / fuse_all_gather (layers.cpp:120-127).
+
+        Per rank x: (B, S/T, K) bf16, w: (K, N_local) bf16, out: (B, S, N_local).
+        A local group takes rank-stacked tensors (T, ...)."""
+        lead = 1 if self.is_local_group else 0
+        B, sl, K = x.shape[lead:]
+        N = w.shape[-1]
+        _check(_lib.tpf_ag_gemm(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B,
+                                sl * self.world, K, N, m, act, _dtype_code(out), _stream_ptr(stream)))
+
+    def gemm_rs(self, x, w, out, kind: int = RING, m: int = 1, wire: int = F32, stream=None) -> None:
+        """row_parallel_forward / fuse_reduce_scatter (layers.cpp:129-138).
+
+        Per rank x: (B, S, K_local) bf16, w: (K_local, N) bf16, out: (B, S/T, N)."""
+        lead = 1 if self.is_local_group else 0
+        B, S, K = x.shape[lead:]
+        N = w.shape[-1]
+        _check(_lib.tpf_gemm_rs(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B, S, K, N,
+                                kind, m, wire, _dtype_code(out), _stream_ptr(stream)))
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.bfloat16:
+        return BF16
+    raise ShapeError(f"unsupported output dtype {t.dtype}")
+
+
+def gemm(a, b, out, stream=None) -> None:
+    """T == 1 degenerate case: out = a @ b on the tcgen05 kernel."""
+    M, K = a.shape
+    N = b.shape[1]
+    _check(_lib.tpf_gemm(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, K, N, _dtype_code(out),
+                         _stream_ptr(stream)))
+
+
+def swiglu(gu, out, stream=None) -> None:
+    rows = gu.numel() // gu.shape[-1]
+    F = gu.shape[-1] // 2
+    _check(_lib.tpf_swiglu(gu.data_ptr(), out.data_ptr(), rows, F, _stream_ptr(stream)))
+
+
+def sym_bytes_ag(world, B, S, K, N_local, m=1) -> int:
+    return int(_lib.tpf_sym_bytes_ag(world, B, S, K, N_local, m))
+
+
+def sym_bytes_rs(world, B, S, K_local, N, m=1, wire=F32) -> int:
+    return int(_lib.tpf_sym_bytes_rs(world, B, S, K_local, N, m, wire))

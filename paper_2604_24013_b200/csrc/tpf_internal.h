@@ -1,0 +1,69 @@
+// Internal (non-ABI) definitions shared by the host runtime (tpf_runtime.cu)
+// and the sm_100a kernels (tpf_kernels.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tpf {
+
+constexpr int kMaxRanks = 8;
+constexpr int BM = 128;          // UMMA M (one CTA)
+constexpr int BN = 256;          // UMMA N
+constexpr int BK = 64;           // 64 bf16 = one 128 B swizzle atom row
+constexpr int kStages = 4;
+constexpr int kThreads = 256;    // 8 warps: TMA, MMA, 2x comm, 4x epilogue
+constexpr int kAStageBytes = BM * BK * 2;  // 16 KiB: also the AG wire "image" unit
+constexpr int kBStageBytes = BN * BK * 2;  // 32 KiB
+constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 + 256;
+
+enum Op : int { OP_RS = 0, OP_AG = 1 };
+enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1 };
+
+// Error record in device memory (first error wins).
+//   [0] code (0 ok, 1 peer-flag timeout, 2 mbarrier timeout)
+//   [1] rank  [2] step  [3] tile / piece  [4] abort flag
+constexpr int kErrWords = 8;
+
+struct KParams {
+  CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks)
+  CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B)
+  int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
+  int T;               // group size
+  int m;               // granularity (ring passes)
+  int direct;          // 1: pairwise rs_direct fold; 0: pipelined (ring / circular)
+  int n_hosted;        // ranks hosted by this launch (1 = one rank per GPU)
+  int rank0;           // rank id of hosted rank 0
+  int ctas_per_rank;   // CTAs serving one hosted rank
+  int act;             // AG epilogue activation (Act)
+  int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
+  int out_f32;         // output dtype: 1 fp32, 0 bf16
+  int nmb_per_batch;   // ceil(Sc / BM)
+  int nmb, nnt, nkb;   // m-blocks, n-tiles, k-blocks per step
+  int nsteps;          // T * m (1 when T == 1)
+  int B;
+  int64_t Sc;          // rows of one sequence chunk, per batch row
+  int64_t K;           // reduction length seen by the GEMM
+  int64_t N;           // output columns
+  int64_t x_rows;      // x rows per batch (RS: S, AG: S/T)
+  int64_t out_rows;    // out rows per batch (RS: S/T, AG: S)
+  const char* x;       // hosted rank 0's x (AG comm warps read it for hop 0)
+  int64_t x_rank_stride;
+  char* out;
+  int64_t out_rank_stride;
+  char* sym[kMaxRanks];     // symmetric base of every rank, mapped in this process
+  int64_t data_off[2];      // per parity: slot data region offset
+  int64_t flag_off[2];      // per parity: flag region offset
+  int64_t slot_bytes;       // one slot (one (pass, iteration) message)
+  int64_t flags_per_slot;
+  uint32_t epoch;
+  int parity;
+  int8_t sched[kMaxRanks][kMaxRanks][3];  // [rank][step] (send, recv, slice)
+  uint32_t* err;
+  int64_t timeout_ns;
+};
+
+void launch_fused(const KParams& p, int grid, cudaStream_t stream);
+int num_sms();
+
+}  // namespace tpf

@@ -1,0 +1,513 @@
+// Persistent, warp-specialised sm_100a kernel family for the CommFuse hot path:
+//
+//   OP_RS  GEMM + decomposed reduce-scatter (fuse_reduce_scatter + row_parallel_forward,
+//          reference collectives.cpp:285-405, layers.cpp:129-138). With T == 1 it is the
+//          plain GEMM (collectives.cpp:379).
+//   OP_AG  decomposed all-gather + GEMM (fuse_all_gather + column_parallel_forward,
+//          reference collectives.cpp:237-279, layers.cpp:120-127).
+//
+// One CTA per SM, 8 warps:
+//   warp 0      TMA producer (A: tensor map or AG wire image, B: W tensor map)
+//   warp 1      tcgen05.mma issuer (128x256x16 bf16 -> fp32 in TMEM, 2 accumulators)
+//   warps 2-3   TMEM allocator / AG ring-forwarding comm warps (NVLink peer stores)
+//   warps 4-7   epilogue: tcgen05.ld -> (+ inbox) -> peer store / output store
+//
+// Work is a static, iteration-major tile list (step = pass * T + iteration), so every
+// cross-rank dependency points to an earlier step and the persistent grid always makes
+// progress. Wire formats are chosen so the consumer does no re-layout:
+//   RS wire  = the TMEM 32x32b fragment image (thread-row interleaved by 16 B column
+//              groups), so each warp-wide 16 B store/load touches 512 contiguous bytes;
+//   AG wire  = the SWIZZLE_128B K-major UMMA operand image of a 128x64 A tile (16 KiB),
+//              so the receiver bulk-copies it straight into a pipeline stage.
+// Flags carry the per-call epoch (monotonic, never reset); slots are double-buffered by
+// epoch parity. Every spin is bounded by a %globaltimer deadline and reports into a
+// device error record instead of trapping.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "tpf_internal.h"
+#include "tpf_ptx.cuh"
+
+namespace tpf {
+
+namespace {
+
+struct Tile {
+  int step, mb, nt, b, row0, valid;
+};
+
+__device__ __forceinline__ Tile get_tile(const KParams& p, int lin) {
+  constexpr int GM = 8;  // grouped raster: 8 m-blocks sweep the n-tiles together
+  const int per_step = p.nmb * p.nnt;
+  Tile t;
+  t.step = lin / per_step;
+  const int rem = lin - t.step * per_step;
+  const int g0 = (rem / (GM * p.nnt)) * GM;
+  const int gm = min(GM, p.nmb - g0);
+  const int r2 = rem - g0 * p.nnt;
+  t.mb = g0 + r2 % gm;
+  t.nt = r2 / gm;
+  t.b = t.mb / p.nmb_per_batch;
+  const int j = t.mb - t.b * p.nmb_per_batch;
+  t.row0 = j * BM;
+  t.valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - t.row0));
+  return t;
+}
+
+__device__ __forceinline__ bool aborted(const KParams& p) {
+  return ld_relaxed_sys(p.err + 4) != 0;
+}
+
+__device__ __noinline__ void record_error(const KParams& p, uint32_t code, int rank, int step,
+                                          int tile) {
+  if (atomicCAS(p.err, 0u, code) == 0u) {
+    p.err[1] = static_cast<uint32_t>(rank);
+    p.err[2] = static_cast<uint32_t>(step);
+    p.err[3] = static_cast<uint32_t>(tile);
+  }
+  atomicExch(p.err + 4, 1u);
+}
+
+// Bounded spin on a peer-written flag (value >= epoch). Returns with acquire
+// semantics; on timeout / abort returns false (the kernel then drains with garbage
+// and the host raises from the error record).
+__device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, int rank,
+                                          int step, int tile) {
+  if (ld_relaxed_sys(f) >= p.epoch) {
+    (void)ld_acquire_sys(f);
+    return true;
+  }
+  const uint64_t t0 = globaltimer();
+  while (true) {
+#pragma unroll 1
+    for (int k = 0; k < 256; ++k) {
+      if (ld_relaxed_sys(f) >= p.epoch) {
+        (void)ld_acquire_sys(f);
+        return true;
+      }
+      __nanosleep(32);
+    }
+    if (aborted(p)) return false;
+    if (globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns)) {
+      record_error(p, 1, rank, step, tile);
+      return false;
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_wait(const KParams& p, uint64_t* bar, uint32_t parity) {
+  if (mbar_try_wait(bar, parity)) return;
+  const uint64_t t0 = globaltimer();
+  while (!mbar_try_wait(bar, parity)) {
+    if (globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns) * 2) {
+      record_error(p, 2, -1, -1, -1);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ char* slot_ptr(const KParams& p, int rank, int slot) {
+  return p.sym[rank] + p.data_off[p.parity] + static_cast<int64_t>(slot) * p.slot_bytes;
+}
+
+__device__ __forceinline__ uint32_t* flag_ptr(const KParams& p, int rank, int slot,
+                                              int64_t idx) {
+  return reinterpret_cast<uint32_t*>(p.sym[rank] + p.flag_off[p.parity]) +
+         static_cast<int64_t>(slot) * p.flags_per_slot + idx;
+}
+
+// Store 32 fp32 accumulator columns of one row to a row-major output.
+__device__ __forceinline__ void store_out_row(const KParams& p, char* row_ptr, int64_t col0,
+                                              const float (&v)[32]) {
+  if (p.out_f32) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      if (col0 + g * 4 < p.N)
+        *reinterpret_cast<float4*>(row_ptr + (col0 + g * 4) * 4) =
+            make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
+  } else {
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      if (col0 + g * 8 < p.N) {
+        uint4 w;
+        w.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+        w.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+        w.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+        w.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+        *reinterpret_cast<uint4*>(row_ptr + (col0 + g * 8) * 2) = w;
+      }
+  }
+}
+
+// RS wire (TMEM-fragment image): sub-chunk j (32 columns), 16 B column group g, row.
+__device__ __forceinline__ int64_t wire_off(int wire_f32, int j, int g, int row) {
+  const int G = wire_f32 ? 8 : 4;
+  return (static_cast<int64_t>(j * G + g) * BM + row) * 16;
+}
+
+__device__ __forceinline__ void wire_store(int wire_f32, char* tile, int j, int row,
+                                           const float (&v)[32]) {
+  if (wire_f32) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g)
+      *reinterpret_cast<float4*>(tile + wire_off(1, j, g, row)) =
+          make_float4(v[g * 4], v[g * 4 + 1], v[g * 4 + 2], v[g * 4 + 3]);
+  } else {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      uint4 w;
+      w.x = pack_bf16x2(v[g * 8 + 0], v[g * 8 + 1]);
+      w.y = pack_bf16x2(v[g * 8 + 2], v[g * 8 + 3]);
+      w.z = pack_bf16x2(v[g * 8 + 4], v[g * 8 + 5]);
+      w.w = pack_bf16x2(v[g * 8 + 6], v[g * 8 + 7]);
+      *reinterpret_cast<uint4*>(tile + wire_off(0, j, g, row)) = w;
+    }
+  }
+}
+
+__device__ __forceinline__ void wire_load(int wire_f32, const char* tile, int j, int row,
+                                          float (&v)[32]) {
+  if (wire_f32) {
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      const float4 w = *reinterpret_cast<const float4*>(tile + wire_off(1, j, g, row));
+      v[g * 4] = w.x; v[g * 4 + 1] = w.y; v[g * 4 + 2] = w.z; v[g * 4 + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const uint4 w = *reinterpret_cast<const uint4*>(tile + wire_off(0, j, g, row));
+      v[g * 8 + 0] = bf16lo(w.x); v[g * 8 + 1] = bf16hi(w.x);
+      v[g * 8 + 2] = bf16lo(w.y); v[g * 8 + 3] = bf16hi(w.y);
+      v[g * 8 + 4] = bf16lo(w.z); v[g * 8 + 5] = bf16hi(w.z);
+      v[g * 8 + 6] = bf16lo(w.w); v[g * 8 + 7] = bf16hi(w.w);
+    }
+  }
+}
+
+// -------------------------------------------------------------- AG forwarding
+// One warp moves one 16 KiB piece (m-block mb, k-block kb) of the travelling chunk to
+// the ring successor. Hop 0 reads this rank's x (row-major) and writes the SWIZZLE_128B
+// operand image; later hops copy the received image verbatim.
+__device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, int mb, int kb,
+                                 int lane) {
+  const int T = p.T;
+  const int pass = slot / (T - 1);
+  const int it = slot - pass * (T - 1);
+  const int dst_rank = p.sched[rank][it][0];
+  char* dst = slot_ptr(p, dst_rank, slot) + (static_cast<int64_t>(mb) * p.nkb + kb) * kAStageBytes;
+  if (it == 0) {
+    const int b = mb / p.nmb_per_batch;
+    const int row0 = (mb - b * p.nmb_per_batch) * BM;
+    const int valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - row0));
+    const char* xb = p.x + h * p.x_rank_stride +
+                     ((static_cast<int64_t>(b) * p.x_rows + pass * p.Sc + row0) * p.K) * 2;
+#pragma unroll 1
+    for (int u0 = 0; u0 < 32; u0 += 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = (u0 + u) * 32 + lane;  // 16 B chunk id in the 128 x 128 B tile
+        const int row = q >> 3, c16 = q & 7;
+        const int64_t col = static_cast<int64_t>(kb) * BK + c16 * 8;
+        v[u] = (row < valid && col < p.K)
+                   ? *reinterpret_cast<const uint4*>(xb + (row * p.K + col) * 2)
+                   : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = (u0 + u) * 32 + lane;
+        const int row = q >> 3, c16 = q & 7;
+        *reinterpret_cast<uint4*>(dst + row * 128 + ((c16 ^ (row & 7)) << 4)) = v[u];
+      }
+    }
+  } else {
+    const uint32_t* f = flag_ptr(p, rank, slot - 1, static_cast<int64_t>(mb) * p.nkb + kb);
+    wait_flag(p, f, rank, slot, mb * p.nkb + kb);
+    __syncwarp();
+    const char* src =
+        slot_ptr(p, rank, slot - 1) + (static_cast<int64_t>(mb) * p.nkb + kb) * kAStageBytes;
+#pragma unroll 1
+    for (int u0 = 0; u0 < 32; u0 += 8) {
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = *reinterpret_cast<const uint4*>(src + ((u0 + u) * 32 + lane) * 16);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        *reinterpret_cast<uint4*>(dst + ((u0 + u) * 32 + lane) * 16) = v[u];
+    }
+  }
+  fence_sys();
+  __syncwarp();
+  if (lane == 0)
+    st_release_sys(flag_ptr(p, dst_rank, slot, static_cast<int64_t>(mb) * p.nkb + kb), p.epoch);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_constant__ KParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + kStages * kAStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * (kAStageBytes + kBStageBytes));
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kStages;
+  uint64_t* tfull = bars + 2 * kStages;
+  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x / p.ctas_per_rank;     // hosted rank served by this CTA
+  const int g = blockIdx.x - h * p.ctas_per_rank; // CTA index within that rank
+  if (h >= p.n_hosted) return;
+  const int rank = p.rank0 + h;
+  const int G = p.ctas_per_rank;
+  const int per_step = p.nmb * p.nnt;
+  const int ntiles = p.nsteps * per_step;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&p.tmap_a);
+    prefetch_tmap(&p.tmap_b);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);
+      mbar_init(tempty + a, 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int lin = g; lin < ntiles; lin += G) {
+        const Tile t = get_tile(p, lin);
+        const int pass = t.step / p.T, it = t.step - pass * p.T;
+        const bool a_from_wire = (p.op == OP_AG) && it > 0;
+        int64_t arow = 0;
+        if (p.op == OP_RS)
+          arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
+        else
+          arow = pass * p.Sc + t.row0;
+        const int aslot = pass * (p.T - 1) + it - 1;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(p, empty + stage, phase ^ 1);
+          uint8_t* sa = smem_a + stage * kAStageBytes;
+          uint8_t* sb = smem_b + stage * kBStageBytes;
+          if (a_from_wire) {
+            const int64_t pidx = static_cast<int64_t>(t.mb) * p.nkb + kb;
+            wait_flag(p, flag_ptr(p, rank, aslot, pidx), rank, t.step, lin);
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(full + stage, kAStageBytes + kBStageBytes);
+            bulk_load(sa, slot_ptr(p, rank, aslot) + pidx * kAStageBytes, kAStageBytes,
+                      full + stage);
+          } else {
+            mbar_arrive_expect_tx(full + stage, kAStageBytes + kBStageBytes);
+            tma_load_4d(sa, &p.tmap_a, full + stage, kb * BK, static_cast<int>(arow), t.b, h);
+          }
+#pragma unroll
+          for (int q = 0; q < BN / 64; ++q)
+            tma_load_3d(sb + q * (64 * BK * 2), &p.tmap_b, full + stage, t.nt * BN + q * 64,
+                        kb * BK, h);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================================================== MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, /*b_mn_major=*/true);
+      int stage = 0;
+      uint32_t phase = 0;
+      int lt = 0;
+      for (int lin = g; lin < ntiles; lin += G, ++lt) {
+        const int a = lt & 1;
+        const uint32_t use = static_cast<uint32_t>(lt >> 1);
+        mbar_wait(p, tempty + a, (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + a * BN;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(p, full + stage, phase);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(smem_a + stage * kAStageBytes);
+          const uint32_t bbase = smem_u32(smem_b + stage * kBStageBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
+            const uint64_t ad = make_sdesc(abase + k * 32, 0, 1024);
+            // B: MN-major SW128; 16 K-rows = 2048 B step; LBO = 64-col block (64 x 128 B),
+            // SBO = 8 K-rows x 128 B.
+            const uint64_t bd = make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
+            mma_bf16(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit(empty + stage);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(tfull + a);
+      }
+    }
+  } else if (warp == 2 || warp == 3) {
+    // ===================================================== AG ring forwarding
+    if (p.op == OP_AG && p.T > 1) {
+      const int cw = warp - 2;
+      const int per_slot = p.nmb * p.nkb;
+      const int npieces = p.m * (p.T - 1) * per_slot;
+      for (int q = g * 2 + cw; q < npieces; q += G * 2) {
+        const int slot = q / per_slot;
+        const int rem = q - slot * per_slot;
+        const int mb = rem / p.nkb;
+        const int kb = rem - mb * p.nkb;
+        ag_forward_piece(p, h, rank, slot, mb, kb, lane);
+      }
+    }
+  } else {
+    // ===================================================== epilogue (warps 4..7)
+    const int ew = warp - 4;
+    const int row = ew * 32 + lane;  // row inside the 128-row tile == TMEM lane
+    char* out_h = p.out + h * p.out_rank_stride;
+    const int64_t esz = p.out_f32 ? 4 : 2;
+    const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
+    int lt = 0;
+    for (int lin = g; lin < ntiles; lin += G, ++lt) {
+      const Tile t = get_tile(p, lin);
+      const int a = lt & 1;
+      const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      mbar_wait(p, tfull + a, use & 1);
+      tc_fence_after();
+      const int pass = t.step / p.T, it = t.step - pass * p.T;
+      const bool valid = row < t.valid;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + a * BN;
+      const int64_t tile_idx = static_cast<int64_t>(t.mb) * p.nnt + t.nt;
+      const int64_t fidx = tile_idx * 4 + ew;
+
+      if (p.op == OP_AG) {
+        const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
+        const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows +
+                             (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
+        char* rp = out_h + orow * p.N * esz;
+        for (int j = 0; j < BN / 32; ++j) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(taddr + j * 32, r);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float x = __uint_as_float(r[c]);
+            v[c] = p.act == ACT_SQUARE ? x * x : x;
+          }
+          if (valid) store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + a);
+        continue;
+      }
+
+      // ------------------------------------------------ OP_RS
+      const bool last = (it == p.T - 1);
+      const int slot_send = pass * (p.T - 1) + it;
+      const int send_rank = p.T > 1 ? p.sched[rank][it][0] : -1;
+      const char* inbox = nullptr;
+      if (!p.direct && it > 0) {
+        const int slot_in = slot_send - 1;
+        wait_flag(p, flag_ptr(p, rank, slot_in, fidx), rank, t.step, lin);
+        inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
+      }
+      if (p.direct && last && p.T > 1) {
+        for (int s = 0; s < p.T - 1; ++s)
+          wait_flag(p, flag_ptr(p, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin);
+      }
+      __syncwarp();
+      char* dst_tile = last ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
+      const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows + pass * p.Sc + t.row0 + row;
+      char* rp = out_h + orow * p.N * esz;
+      for (int j = 0; j < BN / 32; ++j) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + j * 32, r);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
+        if (valid) {
+          if (inbox) {
+            // rs_pipelined: partial += inbox   (collectives.cpp:303)
+            float in[32];
+            wire_load(p.wire_f32, inbox, j, row, in);
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
+          } else if (p.direct && last && p.T > 1) {
+            // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
+            float acc[32];
+            wire_load(p.wire_f32, slot_ptr(p, rank, pass * (p.T - 1)) + tile_idx * tile_bytes, j,
+                      row, acc);
+            for (int s = 1; s < p.T - 1; ++s) {
+              float in[32];
+              wire_load(p.wire_f32,
+                        slot_ptr(p, rank, pass * (p.T - 1) + s) + tile_idx * tile_bytes, j, row,
+                        in);
+#pragma unroll
+              for (int c = 0; c < 32; ++c) acc[c] = acc[c] + in[c];
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c] = acc[c] + v[c];
+          }
+          if (last)
+            store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
+          else
+            wire_store(p.wire_f32, dst_tile, j, row, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty + a);
+      if (!last) {
+        fence_sys();
+        __syncwarp();
+        if (lane == 0) st_release_sys(flag_ptr(p, send_rank, slot_send, fidx), p.epoch);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tpf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSmemBytes);
+    attr_set = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: spins always progress
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, tpf_fused_kernel, p);
+}
+
+}  // namespace tpf

@@ -1,0 +1,529 @@
+// C-ABI implementation (include/tpf.h): communicator + symmetric heap over CUDA
+// IPC, TMA descriptor construction, argument validation mirroring the
+// reference's exceptions, and launch of the persistent fused kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "tpf.h"
+#include "tpf_host.h"
+#include "tpf_internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(const tpf::Status& s) {
+  g_last_error = s.msg;
+  return s.code;
+}
+
+#define TPF_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess)                                                        \
+      return fail(tpf::Status::cuda(std::string(#expr) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+
+constexpr int64_t kFlagBytesPerParity = 1 << 20;  // 256 Ki flags per parity
+constexpr int64_t kDefaultTimeoutNs = 10ll * 1000 * 1000 * 1000;
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int64_t env_timeout_ns() {
+  const char* v = std::getenv("TPF_TIMEOUT_MS");
+  if (v && *v) return static_cast<int64_t>(std::atoll(v)) * 1000 * 1000;
+  return kDefaultTimeoutNs;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// bf16 tensor map with SWIZZLE_128B and zero OOB fill. dims/strides inner -> outer;
+// strides (bytes) for dims 1..rank-1.
+tpf::Status make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                      const uint64_t* strides, const uint32_t* box) {
+  EncodeFn enc = get_encode();
+  if (!enc) return tpf::Status::cuda("cuTensorMapEncodeTiled unavailable (no CUDA driver)");
+  if (reinterpret_cast<uintptr_t>(base) % 16)
+    return tpf::Status::shape("tensor base address must be 16-byte aligned");
+  cuuint64_t d[5], s[4];
+  cuuint32_t b[5], e[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    b[i] = box[i];
+    e[i] = 1;
+    if (i > 0) {
+      s[i - 1] = strides[i - 1];
+      if (strides[i - 1] % 16)
+        return tpf::Status::shape("row pitch must be a multiple of 16 bytes (feature dims % 8 == 0)");
+    }
+  }
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b,
+                   e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return tpf::Status::cuda("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return tpf::Status::ok();
+}
+
+uint32_t* default_err_buffer() {
+  static uint32_t* buf = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    if (cudaMalloc(&buf, tpf::kErrWords * sizeof(uint32_t)) == cudaSuccess)
+      cudaMemset(buf, 0, tpf::kErrWords * sizeof(uint32_t));
+    else
+      buf = nullptr;
+  });
+  return buf;
+}
+
+}  // namespace
+
+struct tpf_comm {
+  int rank = 0;
+  int world = 1;
+  int local_group = 0;          // 1: all ranks hosted by this process (single GPU)
+  size_t sym_bytes = 0;         // per rank
+  char* local = nullptr;        // this process's allocation (all ranks if local_group)
+  char* sym[tpf::kMaxRanks] = {};
+  bool opened[tpf::kMaxRanks] = {};
+  bool peers_ready = false;
+  uint32_t epoch = 0;
+  uint32_t* err = nullptr;      // device error record
+  int64_t timeout_ns = kDefaultTimeoutNs;
+  int device = 0;
+};
+
+namespace {
+
+struct Geometry {
+  int nmb_per_batch, nmb, nnt, nkb;
+  int64_t Sc;
+};
+
+Geometry geometry(int64_t B, int64_t Sc, int64_t K, int64_t N) {
+  Geometry g;
+  g.Sc = Sc;
+  g.nmb_per_batch = static_cast<int>(ceil_div(Sc, tpf::BM));
+  g.nmb = static_cast<int>(B) * g.nmb_per_batch;
+  g.nnt = static_cast<int>(ceil_div(N, tpf::BN));
+  g.nkb = static_cast<int>(ceil_div(K, tpf::BK));
+  return g;
+}
+
+int64_t data_bytes_per_parity(size_t sym_bytes) {
+  return (static_cast<int64_t>(sym_bytes) - 2 * kFlagBytesPerParity) / 2;
+}
+
+struct Call {
+  int op, T, m, direct, act, wire_f32, out_f32, n_hosted, rank0;
+  int64_t B, Sc, K, N, x_rows, out_rows;
+  const void* x;
+  const void* w;
+  void* out;
+  const int32_t* sched;  // T*T*3 or null (T == 1)
+};
+
+tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
+  tpf::KParams p;
+  std::memset(&p, 0, sizeof(p));
+  const Geometry g = geometry(k.B, k.Sc, k.K, k.N);
+  const int R = k.n_hosted;
+  const int64_t x_rank_stride = k.B * k.x_rows * k.K * 2;
+  const int64_t w_rank_stride = k.K * k.N * 2;
+  const int64_t esz = k.out_f32 ? 4 : 2;
+  {
+    const uint64_t dims[4] = {static_cast<uint64_t>(k.K), static_cast<uint64_t>(k.x_rows),
+                              static_cast<uint64_t>(k.B), static_cast<uint64_t>(R)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(k.K * 2),
+                                 static_cast<uint64_t>(k.x_rows * k.K * 2),
+                                 static_cast<uint64_t>(x_rank_stride)};
+    const uint32_t box[4] = {tpf::BK, tpf::BM, 1, 1};
+    tpf::Status s = make_tmap(&p.tmap_a, k.x, 4, dims, strides, box);
+    if (!s.good()) return s;
+  }
+  {
+    const uint64_t dims[3] = {static_cast<uint64_t>(k.N), static_cast<uint64_t>(k.K),
+                              static_cast<uint64_t>(R)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(k.N * 2),
+                                 static_cast<uint64_t>(w_rank_stride)};
+    const uint32_t box[3] = {64, tpf::BK, 1};
+    tpf::Status s = make_tmap(&p.tmap_b, k.w, 3, dims, strides, box);
+    if (!s.good()) return s;
+  }
+  p.op = k.op;
+  p.T = k.T;
+  p.m = k.m;
+  p.direct = k.direct;
+  p.n_hosted = R;
+  p.rank0 = k.rank0;
+  p.act = k.act;
+  p.wire_f32 = k.wire_f32;
+  p.out_f32 = k.out_f32;
+  p.nmb_per_batch = g.nmb_per_batch;
+  p.nmb = g.nmb;
+  p.nnt = g.nnt;
+  p.nkb = g.nkb;
+  p.nsteps = k.T * k.m;
+  p.B = static_cast<int>(k.B);
+  p.Sc = k.Sc;
+  p.K = k.K;
+  p.N = k.N;
+  p.x_rows = k.x_rows;
+  p.out_rows = k.out_rows;
+  p.x = static_cast<const char*>(k.x);
+  p.x_rank_stride = x_rank_stride;
+  p.out = static_cast<char*>(k.out);
+  p.out_rank_stride = k.B * k.out_rows * k.N * esz;
+  p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
+  if (k.T > 1) {
+    for (int r = 0; r < k.T; ++r)
+      for (int i = 0; i < k.T; ++i)
+        for (int f = 0; f < 3; ++f)
+          p.sched[r][i][f] = static_cast<int8_t>(k.sched[(r * k.T + i) * 3 + f]);
+    const int nslots = k.m * (k.T - 1);
+    int64_t slot_bytes, flags_per_slot;
+    if (k.op == tpf::OP_RS) {
+      slot_bytes = static_cast<int64_t>(g.nmb) * g.nnt * tpf::BM * tpf::BN * (k.wire_f32 ? 4 : 2);
+      flags_per_slot = static_cast<int64_t>(g.nmb) * g.nnt * 4;
+    } else {
+      slot_bytes = static_cast<int64_t>(g.nmb) * g.nkb * tpf::kAStageBytes;
+      flags_per_slot = static_cast<int64_t>(g.nmb) * g.nkb;
+    }
+    const int64_t data_cap = data_bytes_per_parity(c->sym_bytes);
+    if (nslots * slot_bytes > data_cap)
+      return tpf::Status::capacity("symmetric heap too small: call needs " +
+                                   std::to_string(2 * (nslots * slot_bytes) + 2 * kFlagBytesPerParity) +
+                                   " bytes per rank, communicator has " + std::to_string(c->sym_bytes));
+    if (nslots * flags_per_slot * 4 > kFlagBytesPerParity)
+      return tpf::Status::capacity("too many flags for one call");
+    for (int r = 0; r < k.T; ++r) p.sym[r] = c->sym[r];
+    p.flag_off[0] = 0;
+    p.flag_off[1] = kFlagBytesPerParity;
+    p.data_off[0] = 2 * kFlagBytesPerParity;
+    p.data_off[1] = 2 * kFlagBytesPerParity + data_cap;
+    p.slot_bytes = slot_bytes;
+    p.flags_per_slot = flags_per_slot;
+    c->epoch += 1;
+    p.epoch = c->epoch;
+    p.parity = static_cast<int>(c->epoch & 1u);
+  } else {
+    p.sched[0][0][0] = -1;
+    p.sched[0][0][1] = -1;
+    p.sched[0][0][2] = 0;
+    p.epoch = 1;
+  }
+  p.err = c ? c->err : default_err_buffer();
+  if (!p.err) return tpf::Status::cuda("no device error buffer (CUDA unavailable)");
+
+  const int sms = tpf::num_sms();
+  if (sms <= 0) return tpf::Status::cuda("no CUDA device");
+  const int per_rank = std::max(1, sms / R);
+  p.ctas_per_rank = per_rank;
+  tpf::launch_fused(p, per_rank * R, stream);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return tpf::Status::cuda(std::string("kernel launch: ") + cudaGetErrorString(e));
+  return tpf::Status::ok();
+}
+
+int hosted(const tpf_comm* c) { return c->local_group ? c->world : 1; }
+
+tpf::Status check_ready(const tpf_comm* c) {
+  if (!c) return tpf::Status::invalid("null communicator");
+  if (c->world > 1 && !c->peers_ready)
+    return tpf::Status::invalid("communicator peers not opened (call tpf_comm_open_peers)");
+  return tpf::Status::ok();
+}
+
+}  // namespace
+
+namespace tpf {
+int num_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+}  // namespace tpf
+
+extern "C" {
+
+int tpf_version(void) { return 1; }
+
+const char* tpf_last_error(void) { return g_last_error.c_str(); }
+
+int tpf_device_sms(void) { return tpf::num_sms(); }
+
+int tpf_ring_indices(int rs, int r, int i, int n, int32_t out[3]) {
+  tpf::Status s = tpf::ring_indices(rs != 0, r, i, n, out);
+  return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_schedule_build(int kind, int n, int32_t* out) {
+  std::vector<int32_t> t;
+  tpf::Status s = tpf::build_schedule(kind, n, t);
+  if (!s.good()) return fail(s);
+  if (!t.empty()) std::memcpy(out, t.data(), t.size() * sizeof(int32_t));
+  return TPF_OK;
+}
+
+int tpf_schedule_check(int kind, int n, const int32_t* table) {
+  tpf::Status s = tpf::check_schedule(kind, n, table);
+  return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out) {
+  if (!out) return fail(tpf::Status::invalid("null output pointer"));
+  if (world < 1 || world > tpf::kMaxRanks || rank < 0 || rank >= world)
+    return fail(tpf::Status::invalid("tpf_comm_create: rank " + std::to_string(rank) +
+                                     " / world " + std::to_string(world) + " out of range (world <= 8)"));
+  if (static_cast<int64_t>(sym_bytes) < 2 * kFlagBytesPerParity + 2 * 4096)
+    sym_bytes = 2 * kFlagBytesPerParity + 2 * 4096;
+  sym_bytes = (sym_bytes + 4095) & ~static_cast<size_t>(4095);
+  tpf_comm* c = new tpf_comm();
+  c->rank = rank;
+  c->world = world;
+  c->sym_bytes = sym_bytes;
+  c->timeout_ns = env_timeout_ns();
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMalloc(&c->local, sym_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->local, 0, sym_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (c->local) cudaFree(c->local);
+    delete c;
+    return fail(tpf::Status::cuda(std::string("tpf_comm_create: ") + cudaGetErrorString(e)));
+  }
+  c->sym[rank] = c->local;
+  c->peers_ready = (world == 1);
+  *out = c;
+  return TPF_OK;
+}
+
+int tpf_comm_ipc_handle(tpf_comm* c, void* handle_out) {
+  if (!c || c->local_group) return fail(tpf::Status::invalid("ipc handle: not a per-process communicator"));
+  cudaIpcMemHandle_t h;
+  static_assert(sizeof(h) == TPF_IPC_HANDLE_BYTES, "IPC handle size");
+  TPF_CUDA_TRY(cudaIpcGetMemHandle(&h, c->local));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return TPF_OK;
+}
+
+int tpf_comm_open_peers(tpf_comm* c, const void* handles) {
+  if (!c || c->local_group) return fail(tpf::Status::invalid("open peers: not a per-process communicator"));
+  const char* hb = static_cast<const char*>(handles);
+  for (int r = 0; r < c->world; ++r) {
+    if (r == c->rank || c->opened[r]) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hb + r * TPF_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    TPF_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->sym[r] = static_cast<char*>(p);
+    c->opened[r] = true;
+  }
+  c->peers_ready = true;
+  return TPF_OK;
+}
+
+int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm** out) {
+  if (!out) return fail(tpf::Status::invalid("null output pointer"));
+  if (world < 1 || world > tpf::kMaxRanks)
+    return fail(tpf::Status::invalid("tpf_comm_create_local_group: world out of range (1..8)"));
+  size_t per = std::max<size_t>(sym_bytes_per_rank, 2 * kFlagBytesPerParity + 2 * 4096);
+  per = (per + 4095) & ~static_cast<size_t>(4095);
+  tpf_comm* c = new tpf_comm();
+  c->rank = 0;
+  c->world = world;
+  c->local_group = 1;
+  c->sym_bytes = per;
+  c->timeout_ns = env_timeout_ns();
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMalloc(&c->local, per * world);
+  if (e == cudaSuccess) e = cudaMemset(c->local, 0, per * world);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (c->local) cudaFree(c->local);
+    delete c;
+    return fail(tpf::Status::cuda(std::string("tpf_comm_create_local_group: ") + cudaGetErrorString(e)));
+  }
+  for (int r = 0; r < world; ++r) c->sym[r] = c->local + per * r;
+  c->peers_ready = true;
+  *out = c;
+  return TPF_OK;
+}
+
+int tpf_comm_destroy(tpf_comm* c) {
+  if (!c) return TPF_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < c->world; ++r)
+    if (c->opened[r]) cudaIpcCloseMemHandle(c->sym[r]);
+  if (c->local) cudaFree(c->local);
+  if (c->err) cudaFree(c->err);
+  delete c;
+  return TPF_OK;
+}
+
+int tpf_comm_rank(const tpf_comm* c) { return c ? c->rank : -1; }
+int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
+
+int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
+  if (!c) return fail(tpf::Status::invalid("null communicator"));
+  c->timeout_ns = ns > 0 ? ns : env_timeout_ns();
+  return TPF_OK;
+}
+
+int tpf_comm_sync(tpf_comm* c, void* stream) {
+  if (!c) return fail(tpf::Status::invalid("null communicator"));
+  TPF_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  uint32_t rec[tpf::kErrWords];
+  TPF_CUDA_TRY(cudaMemcpy(rec, c->err, sizeof(rec), cudaMemcpyDeviceToHost));
+  if (rec[0] != 0) {
+    TPF_CUDA_TRY(cudaMemset(c->err, 0, sizeof(rec)));
+    const int rank = static_cast<int>(rec[1]);
+    std::string what = rec[0] == 1 ? "peer flag wait timed out" : "pipeline barrier timed out";
+    return fail(tpf::Status::peer("rank " + std::to_string(rank) + " failed: " + what +
+                                  " (step " + std::to_string(static_cast<int>(rec[2])) +
+                                  ", tile " + std::to_string(static_cast<int>(rec[3])) + ")"));
+  }
+  return TPF_OK;
+}
+
+int64_t tpf_sym_bytes_ag(int world, int64_t B, int64_t S, int64_t K, int64_t N_local, int m) {
+  if (world <= 1) return 0;
+  const Geometry g = geometry(B, S / world / std::max(m, 1), K, N_local);
+  const int64_t slot = static_cast<int64_t>(g.nmb) * g.nkb * tpf::kAStageBytes;
+  return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(m) * (world - 1) * slot;
+}
+
+int64_t tpf_sym_bytes_rs(int world, int64_t B, int64_t S, int64_t K_local, int64_t N, int m,
+                         int wire_dtype) {
+  if (world <= 1) return 0;
+  const Geometry g = geometry(B, S / world / std::max(m, 1), K_local, N);
+  const int64_t slot =
+      static_cast<int64_t>(g.nmb) * g.nnt * tpf::BM * tpf::BN * (wire_dtype == TPF_F32 ? 4 : 2);
+  return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(m) * (world - 1) * slot;
+}
+
+int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
+             int out_dtype, void* stream) {
+  if (M < 1 || K < 1 || N < 1) return fail(tpf::Status::shape("tpf_gemm: dimensions must be positive"));
+  if (K % 8 || N % 8) return fail(tpf::Status::shape("tpf_gemm: K and N must be multiples of 8"));
+  Call k{};
+  k.op = tpf::OP_RS;
+  k.T = 1; k.m = 1; k.n_hosted = 1;
+  k.out_f32 = out_dtype == TPF_F32;
+  k.B = 1; k.Sc = M; k.K = K; k.N = N; k.x_rows = M; k.out_rows = M;
+  k.x = a; k.w = b; k.out = out;
+  tpf::Status s = launch(nullptr, k, static_cast<cudaStream_t>(stream));
+  return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_ag_gemm(tpf_comm* c, const void* x, const void* w, void* out, int64_t B, int64_t S,
+                int64_t K, int64_t N_local, int m, int act, int out_dtype, void* stream) {
+  // fuse_all_gather argument checks (collectives.cpp:239-248), in reference order.
+  if (m < 1) return fail(tpf::Status::invalid("fuse_all_gather: granularity must be >= 1"));
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  if (B < 1 || S < 1 || K < 1 || N_local < 1)
+    return fail(tpf::Status::shape("column_parallel_forward: dimensions must be positive"));
+  if (S % T)
+    return fail(tpf::Status::invalid("column_parallel_forward: sequence length " + std::to_string(S) +
+                                     " is not divisible by group size " + std::to_string(T)));
+  const int64_t sl = S / T;
+  if (T > 1 && sl % m)
+    return fail(tpf::Status::invalid("fuse_all_gather: slice length " + std::to_string(sl) +
+                                     " is not divisible by granularity " + std::to_string(m)));
+  if (K % 8 || N_local % 8)
+    return fail(tpf::Status::shape("column_parallel_forward: K and N_local must be multiples of 8"));
+  std::vector<int32_t> sched;
+  Call k{};
+  k.op = tpf::OP_AG;
+  k.T = T;
+  k.m = T > 1 ? m : 1;
+  k.act = act;
+  k.out_f32 = out_dtype == TPF_F32;
+  k.n_hosted = hosted(c);
+  k.rank0 = c->local_group ? 0 : c->rank;
+  k.B = B; k.Sc = T > 1 ? sl / m : S; k.K = K; k.N = N_local; k.x_rows = sl; k.out_rows = S;
+  k.x = x; k.w = w; k.out = out;
+  if (T > 1) {
+    sched.resize(static_cast<size_t>(T) * T * 3);
+    for (int r = 0; r < T; ++r)
+      for (int i = 0; i < T; ++i) tpf::ring_indices(false, r, i, T, &sched[(r * T + i) * 3]);
+    k.sched = sched.data();
+  }
+  s = launch(c, k, static_cast<cudaStream_t>(stream));
+  return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B, int64_t S,
+                int64_t K_local, int64_t N, int kind, int m, int wire_dtype, int out_dtype,
+                void* stream) {
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  // fuse_reduce_scatter argument checks (collectives.cpp:365-386), in reference order.
+  if (m < 1) return fail(tpf::Status::invalid("fuse_reduce_scatter: granularity must be >= 1"));
+  if (m > 1 && kind != TPF_RING)
+    return fail(tpf::Status::invalid(
+        "fuse_reduce_scatter: granularity > 1 is supported for the ring schedule only"));
+  std::vector<int32_t> sched;
+  s = tpf::build_schedule(kind, T, sched);
+  if (!s.good()) return fail(s);
+  if (B < 1 || S < 1 || K_local < 1 || N < 1)
+    return fail(tpf::Status::shape("row_parallel_forward: dimensions must be positive"));
+  if (T > 1 && S % (static_cast<int64_t>(T) * m))
+    return fail(tpf::Status::invalid("fuse_reduce_scatter: sequence length " + std::to_string(S) +
+                                     " is not divisible by " + std::to_string(T * m) + " (group size " +
+                                     std::to_string(T) + " x granularity " + std::to_string(m) + ")"));
+  if (K_local % 8 || N % 8)
+    return fail(tpf::Status::shape("row_parallel_forward: K_local and N must be multiples of 8"));
+  Call k{};
+  k.op = tpf::OP_RS;
+  k.T = T;
+  k.m = T > 1 ? m : 1;
+  k.direct = kind == TPF_PAIRWISE;
+  k.wire_f32 = wire_dtype == TPF_F32;
+  k.out_f32 = out_dtype == TPF_F32;
+  k.n_hosted = hosted(c);
+  k.rank0 = c->local_group ? 0 : c->rank;
+  k.B = B; k.Sc = S / (static_cast<int64_t>(T) * k.m); k.K = K_local; k.N = N;
+  k.x_rows = S; k.out_rows = S / T;
+  k.x = x; k.w = w; k.out = out;
+  k.sched = T > 1 ? sched.data() : nullptr;
+  s = launch(c, k, static_cast<cudaStream_t>(stream));
+  return s.good() ? TPF_OK : fail(s);
+}
+
+}  // extern "C"
