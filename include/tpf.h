@@ -96,6 +96,10 @@ int tpf_comm_sync(tpf_comm* c, void* stream);
 /* Test hook (fault injection, fabric_test.cpp:44-58 analogue): shrink the
  * peer-wait timeout (ns). 0 restores the default. */
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns);
+/* Test hook: rank `rank` (-1 = none) stops publishing its peer flags, as if it
+ * had failed mid-collective; its successors time out and tpf_comm_sync reports
+ * TPF_E_PEER naming the waiting rank. */
+int tpf_comm_inject_fault(tpf_comm* c, int rank);
 
 /* -------------------------------------------------------------- fused ops
  * AG-GEMM. Replaces:

@@ -61,6 +61,7 @@ struct KParams {
   int8_t sched[kMaxRanks][kMaxRanks][3];  // [rank][step] (send, recv, slice)
   uint32_t* err;
   int64_t timeout_ns;
+  int fault_rank;   // test hook: this rank never publishes its flags (-1: none)
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);

@@ -241,7 +241,7 @@ __device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, in
   }
   fence_sys();
   __syncwarp();
-  if (lane == 0)
+  if (lane == 0 && rank != p.fault_rank)
     st_release_sys(flag_ptr(p, dst_rank, slot, static_cast<int64_t>(mb) * p.nkb + kb), p.epoch);
 }
 
@@ -479,7 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       if (!last) {
         fence_sys();
         __syncwarp();
-        if (lane == 0) st_release_sys(flag_ptr(p, send_rank, slot_send, fidx), p.epoch);
+        if (lane == 0 && rank != p.fault_rank)
+          st_release_sys(flag_ptr(p, send_rank, slot_send, fidx), p.epoch);
       }
     }
   }

@@ -118,6 +118,7 @@ struct tpf_comm {
   uint32_t* err = nullptr;      // device error record
   int64_t timeout_ns = kDefaultTimeoutNs;
   int device = 0;
+  int fault_rank = -1;
 };
 
 namespace {
@@ -202,6 +203,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.out = static_cast<char*>(k.out);
   p.out_rank_stride = k.B * k.out_rows * k.N * esz;
   p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
+  p.fault_rank = c ? c->fault_rank : -1;
   if (k.T > 1) {
     for (int r = 0; r < k.T; ++r)
       for (int i = 0; i < k.T; ++i)
@@ -399,6 +401,13 @@ int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
   c->timeout_ns = ns > 0 ? ns : env_timeout_ns();
+  return TPF_OK;
+}
+
+int tpf_comm_inject_fault(tpf_comm* c, int rank) {
+  if (!c) return fail(tpf::Status::invalid("null communicator"));
+  if (rank < -1 || rank >= c->world) return fail(tpf::Status::invalid("inject_fault: rank out of range"));
+  c->fault_rank = rank;
   return TPF_OK;
 }
 

@@ -1,0 +1,381 @@
+"""GPU parity of the fused AG-GEMM / GEMM-RS against the oracle (calls go
+through the C ABI of libtpfuse_b200.so).
+
+Tolerances (stated, per north star):
+  * integer data (reference recipe: x in [0,5), w in [-2,2)) — BIT-EXACT vs the
+    fp64 oracle / the reference's own golden outputs (all partial sums are
+    integers < 2^24, exactly representable in bf16 inputs / fp32 accumulators).
+  * random data, fp32 wire — rel_deviation (tensor.cpp:313-318) <= 2e-5 vs the
+    fp64 oracle fed the same bf16-rounded inputs.
+  * random data, bf16 wire — rel_deviation <= (T-1) * 2^-8 + 2e-5 (the running
+    sum is rounded to bf16 once per hop).
+  * full BASELINE sizes — bit-exact vs an fp32 replay of the reference reduction
+    order over this library's own T=1 GEMM partials (size-independent property).
+
+Multi-rank cases run as a single-GPU local group: all T ranks in one persistent
+launch, each rank on its own SM set, peers' symmetric buffers local — the same
+kernel code path that NVLink peers use, with peer pointers into local HBM.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2604_24013_b200 as tpf
+from oracle_lib import Oracle
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+O = Oracle()
+DEV = "cuda:0"
+KINDS = (tpf.RING, tpf.PAIRWISE, tpf.CIRCULAR)
+
+
+def rel_deviation(got, want):
+    diff = np.abs(got - want).max()
+    norm = np.abs(want).max()
+    return diff / norm if norm > 0 else diff
+
+
+def bf16(a):
+    return torch.tensor(np.ascontiguousarray(a), dtype=torch.float32).to(torch.bfloat16)
+
+
+def bf16_round(a):
+    return bf16(a).to(torch.float64).numpy()
+
+
+# ------------------------------------------------------------------ drivers
+def _pad_last(a, n):
+    """Zero-pad the last axis to n (the C ABI needs 16-byte row pitches: dims % 8 == 0;
+    zero padding leaves every product and sum unchanged)."""
+    if a.shape[-1] == n:
+        return a
+    pad = [(0, 0)] * (a.ndim - 1) + [(0, n - a.shape[-1])]
+    return np.pad(a, pad)
+
+
+def _up8(v):
+    return (v + 7) // 8 * 8
+
+
+def run_rs(T, kind, m, x_full, w_full, wire=tpf.F32, out_dtype=torch.float32, comm=None):
+    """Feature-shard x_full (B,S,K) and row-shard w_full (K,N) over T ranks; run GEMM-RS."""
+    B, S, K = x_full.shape
+    N = w_full.shape[1]
+    kl = K // T
+    kp = _up8(kl)
+    x = torch.stack([bf16(_pad_last(x_full[:, :, r * kl:(r + 1) * kl], kp)) for r in range(T)]).to(DEV)
+    w = torch.stack([bf16(_pad_last(w_full[r * kl:(r + 1) * kl].T, kp).T) for r in range(T)]).to(DEV)
+    kl = kp
+    out = torch.full((T, B, S // T, N), float("nan"), device=DEV, dtype=out_dtype)
+    own = comm is None
+    if own:
+        comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, B, S, kl, N, m, wire))
+    comm.gemm_rs(x, w, out, kind=kind, m=m, wire=wire)
+    comm.sync()
+    if own:
+        comm.close()
+    return out.to(torch.float64).cpu().numpy()
+
+
+def run_ag(T, m, x_full, w_full, act=tpf.ACT_NONE, out_dtype=torch.float32, comm=None):
+    """Sequence-slice x_full (B,S,K) and column-shard w_full (K,N); run AG-GEMM."""
+    B, S, K = x_full.shape
+    N = w_full.shape[1]
+    sl, nl = S // T, N // T
+    x = torch.stack([bf16(x_full[:, r * sl:(r + 1) * sl]) for r in range(T)]).to(DEV)
+    w = torch.stack([bf16(w_full[:, r * nl:(r + 1) * nl]) for r in range(T)]).to(DEV)
+    out = torch.full((T, B, S, nl), float("nan"), device=DEV, dtype=out_dtype)
+    own = comm is None
+    if own:
+        comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, B, S, K, nl, m))
+    comm.ag_gemm(x, w, out, m=m, act=act)
+    comm.sync()
+    if own:
+        comm.close()
+    return out.to(torch.float64).cpu().numpy()
+
+
+# ------------------------------------------- SPEC acceptance C1 (golden, exact)
+def golden_cases():
+    z = np.load(os.path.join(HERE, "golden", "cases.npz"))
+    tags = sorted({k.split("/")[0] for k in z.files})
+    return z, tags
+
+
+_Z, _TAGS = golden_cases()
+
+
+@pytest.mark.parametrize("tag", _TAGS)
+def test_c1_row_parallel_exact_vs_reference_golden(tag):
+    t, kind, m = (int(tag.split("_")[i][1:]) for i in range(3))
+    got = run_rs(t, kind, m, _Z[f"{tag}/x2"], _Z[f"{tag}/w2"])
+    assert np.array_equal(got, _Z[f"{tag}/row"]), np.abs(got - _Z[f"{tag}/row"]).max()
+
+
+@pytest.mark.parametrize("tag", _TAGS)
+def test_c1_column_parallel_exact_vs_reference_golden(tag):
+    t, kind, m = (int(tag.split("_")[i][1:]) for i in range(3))
+    got = run_ag(t, m, _Z[f"{tag}/x"], _Z[f"{tag}/up"])
+    assert np.array_equal(got, _Z[f"{tag}/col"])
+
+
+@pytest.mark.parametrize("tag", _TAGS)
+def test_c1_mlp_square_activation(tag):
+    """tpsp_mlp_forward (square activation fused into the AG-GEMM epilogue).
+
+    Stated precision change: the hidden activation is the bf16 operand of the
+    second GEMM. Bit-exact vs the oracle composed with that bf16 rounding;
+    within 2^-8 relative of the reference's fp64 golden output."""
+    t, kind, m = (int(tag.split("_")[i][1:]) for i in range(3))
+    x, up, down = _Z[f"{tag}/x"], _Z[f"{tag}/up"], _Z[f"{tag}/down"]
+    B, S, D = x.shape
+    H = up.shape[1]
+    hid = torch.empty((t, B, S, H // t), device=DEV, dtype=torch.bfloat16)
+    sl, hl = S // t, H // t
+    xs = torch.stack([bf16(x[:, r * sl:(r + 1) * sl]) for r in range(t)]).to(DEV)
+    ups = torch.stack([bf16(up[:, r * hl:(r + 1) * hl]) for r in range(t)]).to(DEV)
+    downs = torch.stack([bf16(down[r * hl:(r + 1) * hl]) for r in range(t)]).to(DEV)
+    out = torch.empty((t, B, S // t, D), device=DEV, dtype=torch.float32)
+    comm = tpf.Communicator.local_group(t, max(tpf.sym_bytes_ag(t, B, S, D, hl, m),
+                                               tpf.sym_bytes_rs(t, B, S, hl, D, m)))
+    comm.ag_gemm(xs, ups, hid, m=m, act=tpf.ACT_SQUARE)
+    comm.gemm_rs(hid, downs, out, kind=kind, m=m)
+    comm.sync()
+    comm.close()
+    got = out.double().cpu().numpy()
+    # oracle with the bf16 hidden rounding
+    h_full = np.concatenate(list(O.column_parallel(t, m, x, up)), axis=-1) ** 2
+    want_bf16 = O.row_parallel(t, kind, m, bf16_round(h_full), down)
+    assert np.array_equal(got, want_bf16)
+    assert rel_deviation(got, _Z[f"{tag}/mlp"]) <= 2.0 ** -8
+
+
+# ------------------------------------------------------ random data tolerance
+@pytest.mark.parametrize("T", [2, 4, 8])
+@pytest.mark.parametrize("kind", KINDS)
+def test_rs_random_fp32_wire(T, kind):
+    if kind == tpf.PAIRWISE and T % 2:
+        pytest.skip()
+    rng = np.random.default_rng(100 + T + kind)
+    B, S, K, N = 2, 64 * T, 96 * T, 264
+    x = bf16_round(rng.standard_normal((B, S, K)))
+    w = bf16_round(rng.standard_normal((K, N)) / np.sqrt(K))
+    got = run_rs(T, kind, 1, x, w)
+    want = O.row_parallel(T, kind, 1, x, w)
+    assert rel_deviation(got, want) <= 2e-5
+
+
+@pytest.mark.parametrize("T", [2, 4, 8])
+def test_rs_random_bf16_wire(T):
+    rng = np.random.default_rng(200 + T)
+    B, S, K, N = 1, 128 * T, 128 * T, 512
+    x = bf16_round(rng.standard_normal((B, S, K)))
+    w = bf16_round(rng.standard_normal((K, N)) / np.sqrt(K))
+    for kind in KINDS:
+        got = run_rs(T, kind, 1, x, w, wire=tpf.BF16)
+        want = O.row_parallel(T, kind, 1, x, w)
+        assert rel_deviation(got, want) <= (T - 1) * 2.0 ** -8 + 2e-5, kind
+
+
+@pytest.mark.parametrize("T,m", [(2, 1), (4, 2), (8, 1)])
+def test_ag_random(T, m):
+    rng = np.random.default_rng(300 + T)
+    B, S, K, N = 2, 96 * T * m, 200, 48 * T
+    x = bf16_round(rng.standard_normal((B, S, K)))
+    w = bf16_round(rng.standard_normal((K, N)) / np.sqrt(K))
+    got = run_ag(T, m, x, w)
+    want = O.column_parallel(T, m, x, w)
+    assert rel_deviation(got, want) <= 2e-5
+
+
+# ------------------------------------------------------------------ edges
+@pytest.mark.parametrize("shape", [
+    (1, 8, 8, 8),          # tiny: one ragged tile, K < 64, N < 256
+    (3, 200, 72, 136),     # B=3, ragged rows (chunk not multiple of 128), N % 256 != 0
+    (1, 64, 136, 264),     # K not multiple of 64, two n-tiles
+])
+@pytest.mark.parametrize("T", [1, 2, 4])
+def test_ragged_shapes_exact(shape, T):
+    B, S, K, N = shape
+    S = S * T * 2
+    K = K * T if K * T % 8 == 0 else K
+    x = O.randint((B, S, K), 0, 5, 7)
+    w = O.randint((K, N), -2, 2, 8)
+    for kind in (tpf.RING, tpf.CIRCULAR):
+        assert np.array_equal(run_rs(T, kind, 2 if kind == tpf.RING and T > 1 else 1, x, w),
+                              O.row_parallel(T, kind, 2 if kind == tpf.RING and T > 1 else 1, x, w))
+    wn = O.randint((K, N * T), -2, 2, 9)
+    assert np.array_equal(run_ag(T, 2, x, wn), O.column_parallel(T, 2 if T > 1 else 1, x, wn))
+
+
+def test_bf16_output_matches_fp32_rounded():
+    rng = np.random.default_rng(5)
+    x = bf16_round(rng.standard_normal((1, 512, 256)))
+    w = bf16_round(rng.standard_normal((256, 256)) / 16)
+    f32 = run_rs(4, tpf.RING, 1, x, w)
+    b16 = run_rs(4, tpf.RING, 1, x, w, out_dtype=torch.bfloat16)
+    assert np.array_equal(b16, bf16_round(f32))
+
+
+def test_repeated_calls_epoch_parity():
+    """Back-to-back calls on one communicator (epoch flags, parity double buffers)."""
+    T, B, S, K, N = 4, 1, 512, 256, 512
+    comm = tpf.Communicator.local_group(T, 2 * tpf.sym_bytes_rs(T, B, S, K // T, N, 1) +
+                                        tpf.sym_bytes_ag(T, B, S, K, N // T, 1))
+    for it in range(6):
+        x = O.randint((B, S, K), 0, 5, 40 + it)
+        w = O.randint((K, N), -2, 2, 50 + it)
+        kind = KINDS[it % 3]
+        assert np.array_equal(run_rs(T, kind, 1, x, w, comm=comm), O.row_parallel(T, kind, 1, x, w))
+        assert np.array_equal(run_ag(T, 1, x, w, comm=comm), O.column_parallel(T, 1, x, w))
+    comm.close()
+
+
+def test_indexed_sum_identity_weights():
+    """collectives_test.cpp:249-268 through the GPU: f = identity (W = I)."""
+    T = 4
+    K = 8 * T
+    # x_r (1, 4, K/T): entry(r, s) = 10r + s in column 0; w_r = I rows of rank r
+    x_full = np.zeros((1, 4, K))
+    for r in range(T):
+        x_full[0, :, r * (K // T)] = [10.0 * r + s for s in range(4)]
+    w_full = np.zeros((K, 8))
+    for r in range(T):
+        w_full[r * (K // T), 0] = 1.0
+    for kind in KINDS:
+        got = run_rs(T, kind, 1, x_full, w_full)
+        assert got[:, 0, 0, 0].tolist() == [60.0 + 4 * s for s in range(T)]
+
+
+# ----------------------------------------------------------- error behaviour
+def test_argument_errors_match_reference():
+    T = 4
+    comm = tpf.Communicator.local_group(T, 1 << 24)
+    x = torch.zeros((T, 1, 64, 16), device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros((T, 16, 32), device=DEV, dtype=torch.bfloat16)
+    out = torch.zeros((T, 1, 16, 32), device=DEV)
+    with pytest.raises(ValueError, match="granularity > 1"):
+        comm.gemm_rs(x, w, out, kind=tpf.PAIRWISE, m=2)
+    with pytest.raises(ValueError, match="granularity must be >= 1"):
+        comm.gemm_rs(x, w, out, m=0)
+    with pytest.raises(ValueError, match="not divisible"):
+        comm.gemm_rs(x[:, :, :62], w, out, m=1)
+    with pytest.raises(ValueError, match="not divisible"):
+        comm.ag_gemm(torch.zeros((T, 1, 3, 16), device=DEV, dtype=torch.bfloat16), w, out, m=2)
+    with pytest.raises(tpf.ShapeError):
+        comm.gemm_rs(torch.zeros((T, 1, 64, 12), device=DEV, dtype=torch.bfloat16),
+                     torch.zeros((T, 12, 32), device=DEV, dtype=torch.bfloat16), out)
+    comm.close()
+    comm3 = tpf.Communicator.local_group(3, 1 << 24)
+    with pytest.raises(ValueError, match="even rank count"):
+        comm3.gemm_rs(torch.zeros((3, 1, 48, 16), device=DEV, dtype=torch.bfloat16),
+                      torch.zeros((3, 16, 32), device=DEV, dtype=torch.bfloat16),
+                      torch.zeros((3, 1, 16, 32), device=DEV), kind=tpf.PAIRWISE)
+    comm3.close()
+
+
+def test_capacity_error():
+    comm = tpf.Communicator.local_group(2, 1 << 20)
+    x = torch.zeros((2, 1, 4096, 64), device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros((2, 64, 4096), device=DEV, dtype=torch.bfloat16)
+    out = torch.zeros((2, 1, 2048, 4096), device=DEV)
+    with pytest.raises(tpf.CapacityError):
+        comm.gemm_rs(x, w, out)
+    comm.close()
+
+
+@pytest.mark.parametrize("op", ["rs", "ag"])
+def test_failed_rank_raises_group_error(op):
+    """A rank that stops publishing (fault injection) surfaces as GroupError, not a hang."""
+    T, B, S, K, N = 4, 1, 512, 256, 256
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, B, S, K, N, 1) + tpf.sym_bytes_ag(T, B, S, K, N, 1))
+    comm.set_timeout_ms(200)
+    comm.inject_fault(2)
+    x = O.randint((B, S, K), 0, 5, 1)
+    w = O.randint((K, N), -2, 2, 2)
+    with pytest.raises(tpf.GroupError, match="rank"):
+        if op == "rs":
+            run_rs(T, tpf.RING, 1, x, w, comm=comm)
+        else:
+            run_ag(T, 1, x, w, comm=comm)
+    comm.inject_fault(-1)
+    # the communicator recovers for the next call
+    assert np.array_equal(run_rs(T, tpf.RING, 1, x, w, comm=comm), O.row_parallel(T, tpf.RING, 1, x, w))
+    comm.close()
+
+
+# -------------------------------------- full BASELINE sizes (property checks)
+def _gemm_f32(a, b):
+    out = torch.empty((a.shape[0], b.shape[1]), device=DEV, dtype=torch.float32)
+    tpf.gemm(a, b, out)
+    return out
+
+
+@pytest.mark.parametrize("wire", [tpf.F32, tpf.BF16])
+@pytest.mark.parametrize("kind", KINDS)
+def test_full_size_cfg2_gemm_rs_bitexact_replay(kind, wire):
+    """Llama-3-8B MLP down-proj GEMM-RS at T=8, S=8192 (BASELINE cfg 2): the fused
+    output equals an fp32 replay of the reference reduction order (App. B) over the
+    T=1 GEMM partials of the same kernel family — bit for bit."""
+    T, S, K, N = 8, 8192, 14336, 4096
+    kl, sc = K // T, S // T
+    g = torch.Generator(device=DEV).manual_seed(kind * 10 + wire)
+    x = (torch.randn((T, 1, S, kl), device=DEV, generator=g)).to(torch.bfloat16)
+    w = (torch.randn((T, kl, N), device=DEV, generator=g) / K ** 0.5).to(torch.bfloat16)
+    out = torch.empty((T, 1, sc, N), device=DEV, dtype=torch.float32)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, 1, S, kl, N, 1, wire))
+    comm.gemm_rs(x, w, out, kind=kind, wire=wire)
+    comm.sync()
+    comm.close()
+    sched = tpf.build_schedule(kind, T)
+    for r in (0, 3, T - 1):  # owners checked (each replay is T GEMMs)
+        parts = {q: _gemm_f32(x[q, 0, r * sc:(r + 1) * sc], w[q]) for q in range(T)}
+        rnd = (lambda v: v.to(torch.bfloat16).float()) if wire == tpf.BF16 else (lambda v: v)
+        if kind == tpf.PAIRWISE:
+            order = [sched[r][i][1] for i in range(T - 1)]
+            acc = rnd(parts[order[0]])
+            for q in order[1:]:
+                acc = acc + rnd(parts[q])
+            acc = acc + parts[r]
+        else:
+            # pipelined: the running sum visits the ranks that compute slice r at steps 0..T-1
+            chain = [next(q for q in range(T) if sched[q][i][2] == r) for i in range(T)]
+            acc = parts[chain[0]]
+            for q in chain[1:]:
+                acc = parts[q] + rnd(acc)
+        assert torch.equal(out[r, 0], acc), (kind, wire, r)
+
+
+def test_full_size_cfg2_ag_gemm_bitexact_vs_gemm():
+    """Llama-3-8B MLP gate||up AG-GEMM at T=8, S=8192: equals the T=1 GEMM on the
+    gathered sequence, bit for bit (AG has no reduction)."""
+    T, S, K, N = 8, 8192, 4096, 28672
+    nl, sl = N // T, S // T
+    g = torch.Generator(device=DEV).manual_seed(1)
+    x = torch.randn((T, 1, sl, K), device=DEV, generator=g).to(torch.bfloat16)
+    w = (torch.randn((T, K, nl), device=DEV, generator=g) / K ** 0.5).to(torch.bfloat16)
+    out = torch.empty((T, 1, S, nl), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, 1, S, K, nl, 1))
+    comm.ag_gemm(x, w, out)
+    comm.sync()
+    comm.close()
+    xg = x.reshape(S, K)
+    for r in (0, 5):
+        ref = torch.empty((S, nl), device=DEV, dtype=torch.bfloat16)
+        tpf.gemm(xg, w[r], ref)
+        assert torch.equal(out[r, 0], ref)
+    # and against cuBLAS fp32 math within tolerance
+    ref32 = xg.float() @ w[0].float()
+    assert (out[0, 0].float() - ref32).abs().max().item() <= 2e-2 * ref32.abs().max().item()
+
+
+def test_swiglu_matches_torch():
+    gu = torch.randn((1000, 2 * 1792), device=DEV).to(torch.bfloat16)
+    out = torch.empty((1000, 1792), device=DEV, dtype=torch.bfloat16)
+    tpf.swiglu(gu, out)
+    g, u = gu.float().chunk(2, dim=-1)
+    ref = torch.nn.functional.silu(g) * u
+    assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
