@@ -1,0 +1,443 @@
+#!/usr/bin/env python
+"""Benchmark: Llama-3-8B TP-SP MLP block, seq 8192, TP = number of GPUs (BASELINE cfg 2).
+
+One step = one forward of the block through this library's fused ops:
+    AG-GEMM   hidden = all_gather_seq(x) @ W_gate||up[r]     (column_parallel_forward)
+    SwiGLU    act    = silu(gate) * up
+    GEMM-RS   y      = reduce_scatter_seq(act @ W_down[r])   (row_parallel_forward)
+x: (1, 8192/T, 4096) bf16 per rank, W_gate||up: (4096, 28672/T), W_down: (14336/T, 4096).
+At N=1 (T=1) both ops are the degenerate plain GEMM (collectives.cpp:242,379).
+
+Prints ONE JSON line (rank 0). `value` = whole-job TFLOP/s with inputs resident in HBM;
+`e2e` = the same through the C-ABI calls with pinned HOST input/output and the copies
+inside the timed region; `roofline` for the dominant kernel (the AG-GEMM launch), timed
+live with CUDA events on its stream; `cpu_baseline` = the reference's own CPU code
+(oracle/_ref, compiled from /root/reference) on a bounded sample, timed on this host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+D_MODEL, FFN, SEQ = 4096, 14336, 8192
+WORKLOAD = "Llama-3-8B TP-SP MLP block (AG-GEMM gate||up -> SwiGLU -> GEMM-RS down), seq 8192"
+METRIC = "AG-GEMM/GEMM-RS TFLOP/s & exposed-comm us at TP=2/4/8; % of roofline"
+
+
+def block_flops(tokens: int) -> float:
+    return 2.0 * tokens * D_MODEL * (2 * FFN) + 2.0 * tokens * FFN * D_MODEL
+
+
+def peaks():
+    p = {"bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "hbm_gbs": 6650.0, "src": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("bf16_tflops", "bf16_tflops_sustained", "hbm_gbs") if k in m})
+        p["src"] = "measured"
+    return p
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.samples, self.proc, self.t0, self.t1 = [], None, None, None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        rows = [s for t, s in self.samples if self.t0 and self.t1 and self.t0 - 0.02 <= t <= self.t1 + 0.02]
+        window = "timed_region"
+        if not rows:
+            rows, window = [s for _, s in self.samples], "whole_run"
+        mhz, maxes, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            f = [v.strip() for v in r.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                mhz.append(float(f[0]))
+                maxes.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not mhz:
+            return None
+        return {"sm_mhz": statistics.median(mhz), "sm_max_mhz": max(maxes), "reasons": sorted(reasons),
+                "samples": len(mhz), "window": window}
+
+
+# ------------------------------------------------------------- CPU reference
+def cpu_reference_sample(threads: int, tokens_per_rank: int, reps: int = 1):
+    """The reference's own CPU path (oracle/_ref = /root/reference/proj/src compiled
+    in place) on a bounded sample of the same block: `threads` simulated TP ranks (one
+    worker thread per rank, fabric.hpp:196-213), tokens_per_rank * threads tokens.
+    Returns per-repetition records."""
+    from oracle_lib import Reference, have_reference
+    if not have_reference():
+        return None
+    R = Reference()
+    t = threads
+    s_cpu = tokens_per_rank * t
+    ag, rs = R.time_ops(t, 1, s_cpu, D_MODEL, 2 * FFN, FFN, D_MODEL, reps)
+    return [{"tokens": s_cpu, "ranks": t, "seconds": a + b, "ag_seconds": a, "rs_seconds": b,
+             "tflops": block_flops(s_cpu) / (a + b) / 1e12} for a, b in zip(ag, rs)]
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    nproc = os.cpu_count() or 1
+    t = max(1, min(8, nproc))
+    recs = cpu_reference_sample(t, 1, args.warmup + args.steps)
+    if recs is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtpfuse_ref.so not built"}))
+        return
+    per_step = recs[args.warmup:]
+    secs = sum(r["seconds"] for r in per_step)
+    flops = sum(block_flops(r["tokens"]) for r in per_step)
+    value = flops / secs / 1e12
+    sample = (f"{per_step[0]['tokens']} tokens of the block per step, {t} simulated TP ranks, one thread "
+              f"each (reference column_parallel_forward + row_parallel_forward, fp64), host nproc={nproc}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / len(per_step), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference randint recipe)",
+        "config": {"workload": WORKLOAD, "tp": world, "seq_len": SEQ, "d_model": D_MODEL, "ffn": FFN,
+                   "global_batch": 1, "parallelism": f"tp{world}-sp (reference: {t} rank threads)"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": t, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_24013_b200 as tpf
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    T = world
+    S_l, F_l = SEQ // T, FFN // T
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    x = torch.randn((1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
+    w_gu = (torch.randn((D_MODEL, 2 * F_l), device=dev, generator=g) / D_MODEL ** 0.5).to(torch.bfloat16)
+    w_dn = (torch.randn((F_l, D_MODEL), device=dev, generator=g) / FFN ** 0.5).to(torch.bfloat16)
+    hid = torch.empty((1, SEQ, 2 * F_l), device=dev, dtype=torch.bfloat16)
+    act = torch.empty((1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
+    stream = torch.cuda.current_stream(dev)
+
+    comm = None
+    if T > 1:
+        need = max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
+                   tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16))
+        comm = tpf.Communicator.from_process_group(need)
+
+    def ag():
+        if comm is None:
+            tpf.gemm(x.view(S_l, D_MODEL), w_gu, hid.view(SEQ, 2 * F_l), stream=stream)
+        else:
+            comm.ag_gemm(x, w_gu, hid, stream=stream)
+
+    def sw():
+        tpf.swiglu(hid, act, stream=stream)
+
+    def rs():
+        if comm is None:
+            tpf.gemm(act.view(SEQ, F_l), w_dn, y.view(S_l, D_MODEL), stream=stream)
+        else:
+            comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        ag(); sw(); rs()
+    if comm:
+        comm.sync(stream)
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region (device-resident inputs); per-kernel events on the launch stream
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    n = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    if sampler:
+        sampler.mark_start()
+    for i in range(n):
+        ev[i][0].record(stream)
+        ag()
+        ev[i][1].record(stream)
+        sw()
+        ev[i][2].record(stream)
+        rs()
+        ev[i][3].record(stream)
+    torch.cuda.synchronize(dev)
+    if sampler:
+        sampler.mark_end()
+    barrier()
+    if comm:
+        comm.sync(stream)
+    total_ms = ev[0][0].elapsed_time(ev[-1][3])
+    ag_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / n
+    sw_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / n
+    rs_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / n
+    ms_step = max_over_ranks(total_ms / n)
+    ag_ms, sw_ms, rs_ms = max_over_ranks(ag_ms), max_over_ranks(sw_ms), max_over_ranks(rs_ms)
+    clocks = sampler.stop() if sampler else None
+    flops_step = block_flops(SEQ)  # whole job
+    value = flops_step / (ms_step * 1e-3) / 1e12
+
+    # ---- e2e through the public API with pinned host buffers (copies timed)
+    x_host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    x_host.copy_(x.cpu())
+    y_host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        x.copy_(x_host, non_blocking=True)
+        ag(); sw(); rs()
+        y_host.copy_(y, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n)
+    e2e_value = flops_step / (e2e_ms * 1e-3) / 1e12
+    h2d = x_host.numel() * x_host.element_size() * world
+    d2h = y_host.numel() * y_host.element_size() * world
+
+    # ---- non-overlapped baseline: cuBLAS (+ NCCL all-gather / reduce-scatter for T > 1)
+    base_ms = None
+    try:
+        xg = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
+        yfull = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
+
+        def base_step():
+            if T > 1:
+                dist.all_gather_into_tensor(xg, x)
+            else:
+                xg.copy_(x)
+            h = torch.matmul(xg.view(SEQ, D_MODEL), w_gu)
+            gt, up = h.chunk(2, dim=-1)
+            a = torch.nn.functional.silu(gt) * up
+            torch.matmul(a, w_dn, out=yfull.view(SEQ, D_MODEL))
+            if T > 1:
+                dist.reduce_scatter_tensor(y, yfull)
+        for _ in range(max(2, args.warmup)):
+            base_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(n):
+            base_step()
+        b1.record(stream)
+        torch.cuda.synchronize(dev)
+        base_ms = max_over_ranks(b0.elapsed_time(b1) / n)
+    except Exception as exc:  # baseline is informative only
+        base_ms = None
+        print(f"[bench] baseline failed: {exc}", file=sys.stderr)
+
+    # ---- single-GPU emulation of TP=8 (one persistent launch hosts all 8 ranks)
+    emu = None
+    if world == 1 and args.emulate_tp > 1:
+        emu = emulated_block(args, dev, stream, args.emulate_tp)
+
+    if rank != 0:
+        return
+    pk = peaks()
+    ag_flops = 2.0 * SEQ * D_MODEL * (2 * F_l)  # per rank per launch
+    achieved = ag_flops / (ag_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get(f"ag_gemm_tp{T}")
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        nproc = os.cpu_count() or 1
+        cbs = cpu_reference_sample(max(1, min(8, nproc)), 8)
+        cb = cbs[0] if cbs else None
+        if cb:
+            cpu = {"value": cb["tflops"], "unit": "TFLOP/s", "cores": cb["ranks"], "kind": "reference",
+                   "sample": f"{cb['tokens']} tokens of the block ({cb['ranks']} simulated TP ranks, "
+                             f"one thread each), {cb['seconds']:.1f} s of reference CPU work, host nproc={nproc}"}
+    out = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOP/s",
+        "n_gpus": world,
+        "steps": n,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded randn, random-init weights of the Llama-3-8B MLP shapes)",
+        "config": {"workload": WORKLOAD, "tp": T, "seq_len": SEQ, "global_batch": 1, "d_model": D_MODEL,
+                   "ffn": FFN, "parallelism": f"tp{T}-sp" if T > 1 else "tp1 (degenerate: plain GEMMs)",
+                   "rs_schedule": "ring", "rs_wire": "bf16",
+                   "l2": "no flush: per-step working set ~1.0 GB (weights 352 MB + hidden 470 MB) > 126 MB L2"},
+        "gpu_launches": 3 * n,
+        "ops": {
+            "ag_gemm": {"ms": ag_ms, "tflops": 2.0 * SEQ * D_MODEL * 2 * FFN / (ag_ms * 1e-3) / 1e12},
+            "swiglu": {"ms": sw_ms, "gbs": 3.0 * SEQ * F_l * 2 * T / (sw_ms * 1e-3) / 1e9},
+            "gemm_rs": {"ms": rs_ms, "tflops": 2.0 * SEQ * FFN * D_MODEL / (rs_ms * 1e-3) / 1e12},
+            "exposed_comm_us": 0.0 if T == 1 else None,
+        },
+        "roofline": {"kernel": "tpf_fused_kernel (AG-GEMM gate||up)", "bound": "tensor",
+                     "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
+                     "peak_src": f"{pk['src']} burst; frac vs sustained {pk['bf16_tflops_sustained']}: "
+                                 f"{achieved / pk['bf16_tflops_sustained']:.3f}",
+                     "flops_per_launch": ag_flops},
+        "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_ms},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    if base_ms:
+        out["baseline_cublas_nccl"] = {"ms_per_step": base_ms, "tflops": flops_step / (base_ms * 1e-3) / 1e12,
+                                       "speedup_ours": base_ms / ms_step}
+    if emu:
+        out["emulated"] = emu
+    print(json.dumps(out))
+
+
+def emulated_block(args, dev, stream, T):
+    """cfg2 block at TP=T with all T ranks hosted on this GPU in one launch per op
+    (each rank on 148/T SMs; 'peer' buffers in local HBM). Same FLOPs as the T=1 run,
+    so the ratio exposes the fused protocol's overhead (flags, wire copies, forwarding)."""
+    import torch
+
+    import paper_2604_24013_b200 as tpf
+    S_l, F_l = SEQ // T, FFN // T
+    g = torch.Generator(device=dev).manual_seed(7)
+    x = torch.randn((T, 1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
+    w_gu = (torch.randn((T, D_MODEL, 2 * F_l), device=dev, generator=g) / 64).to(torch.bfloat16)
+    w_dn = (torch.randn((T, F_l, D_MODEL), device=dev, generator=g) / 120).to(torch.bfloat16)
+    hid = torch.empty((T, 1, SEQ, 2 * F_l), device=dev, dtype=torch.bfloat16)
+    act = torch.empty((T, 1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((T, 1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
+                                               tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
+
+    def step():
+        comm.ag_gemm(x, w_gu, hid, stream=stream)
+        tpf.swiglu(hid, act, stream=stream)
+        comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    comm.sync(stream)
+    n = args.steps
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    for i in range(n):
+        ev[i][0].record(stream)
+        comm.ag_gemm(x, w_gu, hid, stream=stream)
+        ev[i][1].record(stream)
+        tpf.swiglu(hid, act, stream=stream)
+        ev[i][2].record(stream)
+        comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
+        ev[i][3].record(stream)
+    comm.sync(stream)
+    total = ev[0][0].elapsed_time(ev[-1][3]) / n
+    ag = sum(e[0].elapsed_time(e[1]) for e in ev) / n
+    rs = sum(e[2].elapsed_time(e[3]) for e in ev) / n
+    comm.close()
+    return {"tp": T, "note": "all ranks on ONE GPU (local group); wire traffic goes through local HBM, not NVLink",
+            "ms_per_step": total, "tflops": block_flops(SEQ) / (total * 1e-3) / 1e12,
+            "ag_gemm_ms": ag, "gemm_rs_ms": rs}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--emulate-tp", type=int, default=8, help="single-GPU local-group TP (N=1 only; 0 = off)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference sample")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

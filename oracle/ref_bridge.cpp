@@ -200,37 +200,40 @@ int ref_mlp_square(int t, int kind, int m, int64_t b, int64_t s, int64_t d, int6
   });
 }
 
-// Timing leg for the CPU baseline: runs row_parallel_forward and
-// column_parallel_forward of the reference on integer data with T rank
-// threads (the reference's own concurrency: one worker per rank,
-// fabric.hpp:196-213). Inputs are generated inside (randint recipe) and are
-// not timed. Returns wall seconds of each op in secs[0] (AG) / secs[1] (RS).
+// Timing leg for the CPU baseline / reference arm: runs the reference's
+// column_parallel_forward (AG-GEMM, K_ag x N_ag) and row_parallel_forward
+// (GEMM-RS, K_rs x N_rs, ring) on integer data with T rank threads (the
+// reference's own concurrency: one worker per rank, fabric.hpp:196-213).
+// Inputs are generated once, outside the timed region; each of `reps`
+// repetitions is timed with steady_clock around spawn_group (the reference's
+// own bench pattern, experiment.cpp:755-763). ag_secs/rs_secs: reps entries.
 int ref_time_ops(int t, int64_t b, int64_t s, int64_t k_ag, int64_t n_ag, int64_t k_rs,
-                 int64_t n_rs, double* secs) {
+                 int64_t n_rs, int reps, double* ag_secs, double* rs_secs) {
   return guarded([&] {
     using clk = std::chrono::steady_clock;
     const tpfuse::Tensor x_ag = tpfuse::randint_fill(b, s, k_ag, 0, 5, 2);
     const tpfuse::ShardedLinear w_ag = tpfuse::ShardedLinear::split_columns(
         tpfuse::randint_matrix(k_ag, n_ag, -2, 2, 1), t);
     const auto slices = tpfuse::split_seq(x_ag, t);
-    auto t0 = clk::now();
-    tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
-      return tpfuse::column_parallel_forward(ep, slices[ep.rank()], w_ag, 1);
-    });
-    auto t1 = clk::now();
     const int64_t kl = k_rs / t;
     std::vector<tpfuse::Tensor> xs;
     for (int r = 0; r < t; ++r) xs.push_back(tpfuse::randint_fill(b, s, kl, 0, 5, 10 + r));
     const tpfuse::ShardedLinear w_rs = tpfuse::ShardedLinear::split_rows(
         tpfuse::randint_matrix(k_rs, n_rs, -2, 2, 3), t);
     const tpfuse::Schedule ring = tpfuse::build_schedule(tpfuse::ScheduleKind::Ring, t);
-    auto t2 = clk::now();
-    tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
-      return tpfuse::row_parallel_forward(ep, xs[ep.rank()], w_rs, ring, 1);
-    });
-    auto t3 = clk::now();
-    secs[0] = std::chrono::duration<double>(t1 - t0).count();
-    secs[1] = std::chrono::duration<double>(t3 - t2).count();
+    for (int i = 0; i < reps; ++i) {
+      auto t0 = clk::now();
+      tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
+        return tpfuse::column_parallel_forward(ep, slices[ep.rank()], w_ag, 1);
+      });
+      auto t1 = clk::now();
+      tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
+        return tpfuse::row_parallel_forward(ep, xs[ep.rank()], w_rs, ring, 1);
+      });
+      auto t2 = clk::now();
+      ag_secs[i] = std::chrono::duration<double>(t1 - t0).count();
+      rs_secs[i] = std::chrono::duration<double>(t2 - t1).count();
+    }
   });
 }
 

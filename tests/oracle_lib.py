@@ -151,7 +151,7 @@ class Reference:
         L.ref_row_parallel.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D]
         L.ref_fuse_rs_identity.argtypes = [C.c_int] * 3 + [_i64] * 3 + [_D, _D]
         L.ref_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
-        L.ref_time_ops.argtypes = [C.c_int] + [_i64] * 6 + [_D]
+        L.ref_time_ops.argtypes = [C.c_int] + [_i64] * 6 + [C.c_int, _D, _D]
         self.L = L
 
     def _chk(self, rc):
@@ -210,7 +210,9 @@ class Reference:
                                         np.ascontiguousarray(down).reshape(-1), out))
         return out.reshape(t, b, s // t, d)
 
-    def time_ops(self, t, b, s, k_ag, n_ag, k_rs, n_rs):
-        secs = np.zeros(2, np.float64)
-        self._chk(self.L.ref_time_ops(t, b, s, k_ag, n_ag, k_rs, n_rs, secs))
-        return float(secs[0]), float(secs[1])
+    def time_ops(self, t, b, s, k_ag, n_ag, k_rs, n_rs, reps=1):
+        """Per-repetition wall seconds of the reference's AG-GEMM and GEMM-RS."""
+        ag = np.zeros(reps, np.float64)
+        rs = np.zeros(reps, np.float64)
+        self._chk(self.L.ref_time_ops(t, b, s, k_ag, n_ag, k_rs, n_rs, reps, ag, rs))
+        return ag.tolist(), rs.tolist()
