@@ -8,14 +8,15 @@
 namespace tpf {
 
 constexpr int kMaxRanks = 8;
-constexpr int BM = 128;          // UMMA M (one CTA)
-constexpr int BN = 256;          // UMMA N
+constexpr int BM = 128;          // rows per CTA; the CTA pair computes 256 x BN (UMMA M = 256)
+constexpr int BN = 256;          // UMMA N (each CTA of the pair stages BN/2 columns of B)
 constexpr int BK = 64;           // 64 bf16 = one 128 B swizzle atom row
-constexpr int kStages = 4;
+constexpr int kStages = 6;
 constexpr int kThreads = 256;    // 8 warps: TMA, MMA, 2x comm, 4x epilogue
-constexpr int kAStageBytes = BM * BK * 2;  // 16 KiB: also the AG wire "image" unit
-constexpr int kBStageBytes = BN * BK * 2;  // 32 KiB
-constexpr int kSmemBytes = kStages * (kAStageBytes + kBStageBytes) + 1024 + 256;
+constexpr int kAStageBytes = BM * BK * 2;        // 16 KiB: also the AG wire "image" unit
+constexpr int kBStageBytes = (BN / 2) * BK * 2;  // 16 KiB: this CTA's half of B
+constexpr int kStageBytes = kAStageBytes + kBStageBytes;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
 enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1 };
@@ -28,18 +29,21 @@ constexpr int kErrWords = 8;
 struct KParams {
   CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks)
   CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B)
+  CUtensorMap tmap_wire;  // AG wire images (128 B, 128 rows, image, slot, hosted rank), no swizzle
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
   int T;               // group size
   int m;               // granularity (ring passes)
   int direct;          // 1: pairwise rs_direct fold; 0: pipelined (ring / circular)
   int n_hosted;        // ranks hosted by this launch (1 = one rank per GPU)
   int rank0;           // rank id of hosted rank 0
-  int ctas_per_rank;   // CTAs serving one hosted rank
+  int ctas_per_rank;   // CTAs serving one hosted rank (even: CTA pairs)
+  int group_m;         // raster: m-block pairs that sweep the n-tiles together
   int act;             // AG epilogue activation (Act)
   int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
   int out_f32;         // output dtype: 1 fp32, 0 bf16
   int nmb_per_batch;   // ceil(Sc / BM)
   int nmb, nnt, nkb;   // m-blocks, n-tiles, k-blocks per step
+  int npairs;          // ceil(nmb / 2): m-block pairs (one per CTA pair)
   int nsteps;          // T * m (1 when T == 1)
   int B;
   int64_t Sc;          // rows of one sequence chunk, per batch row
@@ -65,6 +69,7 @@ struct KParams {
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
+int max_pairs();
 int num_sms();
 
 }  // namespace tpf

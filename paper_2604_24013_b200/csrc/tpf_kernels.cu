@@ -6,11 +6,14 @@
 //   OP_AG  decomposed all-gather + GEMM (fuse_all_gather + column_parallel_forward,
 //          reference collectives.cpp:237-279, layers.cpp:120-127).
 //
-// One CTA per SM, 8 warps:
-//   warp 0      TMA producer (A: tensor map or AG wire image, B: W tensor map)
-//   warp 1      tcgen05.mma issuer (128x256x16 bf16 -> fp32 in TMEM, 2 accumulators)
+// CTA pairs (cluster of 2, tcgen05 cta_group::2), one CTA per SM, 8 warps each:
+//   warp 0      TMA producer: this CTA's 128-row A block (tensor map or AG wire image)
+//               and its half of the 256-column B tile; completion lands on the leader's
+//               full barrier
+//   warp 1      (leader CTA only) tcgen05.mma.cta_group::2, 256x256x16 bf16 -> fp32, two
+//               TMEM accumulators; commits multicast to both CTAs' barriers
 //   warps 2-3   TMEM allocator / AG ring-forwarding comm warps (NVLink peer stores)
-//   warps 4-7   epilogue: tcgen05.ld -> (+ inbox) -> peer store / output store
+//   warps 4-7   epilogue: tcgen05.ld of this CTA's 128 rows -> (+ inbox) -> peer / output
 //
 // Work is a static, iteration-major tile list (step = pass * T + iteration), so every
 // cross-rank dependency points to an earlier step and the persistent grid always makes
@@ -34,20 +37,25 @@ namespace tpf {
 namespace {
 
 struct Tile {
-  int step, mb, nt, b, row0, valid;
+  int step, mb, nt, b, row0, valid;  // mb: THIS CTA's m-block; valid rows (0 if mb >= nmb)
 };
 
-__device__ __forceinline__ Tile get_tile(const KParams& p, int lin) {
-  constexpr int GM = 8;  // grouped raster: 8 m-blocks sweep the n-tiles together
-  const int per_step = p.nmb * p.nnt;
+// Pair-tile raster: step-major; inside a step, group_m m-block pairs sweep the n-tiles.
+__device__ __forceinline__ Tile get_tile(const KParams& p, int lin, int cta) {
+  const int GM = p.group_m;
+  const int per_step = p.npairs * p.nnt;
   Tile t;
   t.step = lin / per_step;
   const int rem = lin - t.step * per_step;
   const int g0 = (rem / (GM * p.nnt)) * GM;
-  const int gm = min(GM, p.nmb - g0);
+  const int gm = min(GM, p.npairs - g0);
   const int r2 = rem - g0 * p.nnt;
-  t.mb = g0 + r2 % gm;
+  t.mb = 2 * (g0 + r2 % gm) + cta;
   t.nt = r2 / gm;
+  if (t.mb >= p.nmb) {
+    t.b = 0; t.row0 = 0; t.valid = 0;
+    return t;
+  }
   t.b = t.mb / p.nmb_per_batch;
   const int j = t.mb - t.b * p.nmb_per_batch;
   t.row0 = j * BM;
@@ -253,55 +261,62 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + kStages * kAStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * (kAStageBytes + kBStageBytes));
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kStages;
-  uint64_t* tfull = bars + 2 * kStages;
-  uint64_t* tempty = bars + 2 * kStages + 2;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* full = bars;                  // leader: 2 arrivals + 2 x stage tx bytes
+  uint64_t* empty = bars + kStages;       // per CTA: 1 (leader's multicast commit)
+  uint64_t* tfull = bars + 2 * kStages;   // per CTA: 1 (leader's multicast commit)
+  uint64_t* tempty = bars + 2 * kStages + 2;  // leader: 8 epilogue warps of the pair
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int h = blockIdx.x / p.ctas_per_rank;     // hosted rank served by this CTA
-  const int g = blockIdx.x - h * p.ctas_per_rank; // CTA index within that rank
-  if (h >= p.n_hosted) return;
+  const int cta = static_cast<int>(cluster_ctarank());
+  const bool leader = cta == 0;
+  const int h = blockIdx.x / p.ctas_per_rank;      // hosted rank served by this CTA
+  const int g = blockIdx.x - h * p.ctas_per_rank;  // CTA index within that rank
   const int rank = p.rank0 + h;
   const int G = p.ctas_per_rank;
-  const int per_step = p.nmb * p.nnt;
+  const int gp = g >> 1, GP = G >> 1;  // pair index / pairs per rank
+  const int per_step = p.npairs * p.nnt;
   const int ntiles = p.nsteps * per_step;
+  const bool active = h < p.n_hosted;  // (grid is sized exactly; kept for safety)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tmap_a);
     prefetch_tmap(&p.tmap_b);
+    if (p.op == OP_AG && p.T > 1) prefetch_tmap(&p.tmap_wire);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full + s, 1);
+      mbar_init(full + s, 2);
       mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
-      mbar_init(tempty + a, 4);
+      mbar_init(tempty + a, 8);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<512>(tmem_holder);
+  if (warp == 2) tmem_alloc_2sm<512>(tmem_holder);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  if (warp == 0) {
-    // ===================================================== TMA producer
+  if (!active) {
+  } else if (warp == 0) {
+    // ===================================================== TMA producer (both CTAs)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int lin = g; lin < ntiles; lin += G) {
-        const Tile t = get_tile(p, lin);
+      for (int lin = gp; lin < ntiles; lin += GP) {
+        const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
         const bool a_from_wire = (p.op == OP_AG) && it > 0;
-        int64_t arow = 0;
-        if (p.op == OP_RS)
+        int64_t arow;
+        if (t.valid == 0)
+          arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
+        else if (p.op == OP_RS)
           arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
         else
           arow = pass * p.Sc + t.row0;
@@ -310,33 +325,36 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           mbar_wait(p, empty + stage, phase ^ 1);
           uint8_t* sa = smem_a + stage * kAStageBytes;
           uint8_t* sb = smem_b + stage * kBStageBytes;
-          if (a_from_wire) {
-            const int64_t pidx = static_cast<int64_t>(t.mb) * p.nkb + kb;
-            wait_flag(p, flag_ptr(p, rank, aslot, pidx), rank, t.step, lin);
+          const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
+          const int img = t.mb * p.nkb + kb;
+          if (a_from_wire && t.valid) {
+            wait_flag(p, flag_ptr(p, rank, aslot, img), rank, t.step, lin);
             fence_proxy_async_global();
-            mbar_arrive_expect_tx(full + stage, kAStageBytes + kBStageBytes);
-            bulk_load(sa, slot_ptr(p, rank, aslot) + pidx * kAStageBytes, kAStageBytes,
-                      full + stage);
-          } else {
-            mbar_arrive_expect_tx(full + stage, kAStageBytes + kBStageBytes);
-            tma_load_4d(sa, &p.tmap_a, full + stage, kb * BK, static_cast<int>(arow), t.b, h);
           }
+          if (leader)
+            mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
+          else
+            mbar_arrive_cluster(fb);
+          if (a_from_wire)
+            tma_load_2sm_5d(sa, &p.tmap_wire, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
+          else
+            tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
 #pragma unroll
-          for (int q = 0; q < BN / 64; ++q)
-            tma_load_3d(sb + q * (64 * BK * 2), &p.tmap_b, full + stage, t.nt * BN + q * 64,
-                        kb * BK, h);
+          for (int q = 0; q < BN / 128; ++q)
+            tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                            kb * BK, h);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===================================================== MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(BM, BN, /*b_mn_major=*/true);
+    // ===================================================== MMA issuer (leader CTA)
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/true);
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
-      for (int lin = g; lin < ntiles; lin += G, ++lt) {
+      for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
         const int a = lt & 1;
         const uint32_t use = static_cast<uint32_t>(lt >> 1);
         mbar_wait(p, tempty + a, (use & 1) ^ 1);
@@ -351,15 +369,15 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           for (int k = 0; k < BK / 16; ++k) {
             // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
             const uint64_t ad = make_sdesc(abase + k * 32, 0, 1024);
-            // B: MN-major SW128; 16 K-rows = 2048 B step; LBO = 64-col block (64 x 128 B),
-            // SBO = 8 K-rows x 128 B.
+            // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
+            // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
             const uint64_t bd = make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
-            mma_bf16(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
-          mma_commit(empty + stage);
+          mma_commit_2sm(empty + stage, 0x3);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        mma_commit(tfull + a);
+        mma_commit_2sm(tfull + a, 0x3);
       }
     }
   } else if (warp == 2 || warp == 3) {
@@ -379,19 +397,22 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   } else {
     // ===================================================== epilogue (warps 4..7)
     const int ew = warp - 4;
-    const int row = ew * 32 + lane;  // row inside the 128-row tile == TMEM lane
+    const int row = ew * 32 + lane;  // row inside this CTA's 128-row block == TMEM lane
     char* out_h = p.out + h * p.out_rank_stride;
     const int64_t esz = p.out_f32 ? 4 : 2;
     const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(tempty + 1), 0);
     int lt = 0;
-    for (int lin = g; lin < ntiles; lin += G, ++lt) {
-      const Tile t = get_tile(p, lin);
+    for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+      const Tile t = get_tile(p, lin, cta);
       const int a = lt & 1;
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
       mbar_wait(p, tfull + a, use & 1);
       tc_fence_after();
       const int pass = t.step / p.T, it = t.step - pass * p.T;
       const bool valid = row < t.valid;
+      const bool tile_live = t.valid > 0;
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + a * BN;
       const int64_t tile_idx = static_cast<int64_t>(t.mb) * p.nnt + t.nt;
       const int64_t fidx = tile_idx * 4 + ew;
@@ -415,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty + a);
+        if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
         continue;
       }
 
@@ -424,17 +445,18 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const int slot_send = pass * (p.T - 1) + it;
       const int send_rank = p.T > 1 ? p.sched[rank][it][0] : -1;
       const char* inbox = nullptr;
-      if (!p.direct && it > 0) {
+      if (tile_live && !p.direct && it > 0) {
         const int slot_in = slot_send - 1;
         wait_flag(p, flag_ptr(p, rank, slot_in, fidx), rank, t.step, lin);
         inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
       }
-      if (p.direct && last && p.T > 1) {
+      if (tile_live && p.direct && last && p.T > 1) {
         for (int s = 0; s < p.T - 1; ++s)
           wait_flag(p, flag_ptr(p, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin);
       }
       __syncwarp();
-      char* dst_tile = last ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
+      char* dst_tile =
+          (last || !tile_live) ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
       const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows + pass * p.Sc + t.row0 + row;
       char* rp = out_h + orow * p.N * esz;
       for (int j = 0; j < BN / 32; ++j) {
@@ -475,8 +497,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + a);
-      if (!last) {
+      if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
+      if (!last && tile_live) {
         fence_sys();
         __syncwarp();
         if (lane == 0 && rank != p.fault_rank)
@@ -486,9 +508,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   }
 
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc<512>(tmem_base);
+  if (warp == 2) tmem_dealloc_2sm<512>(tmem_base);
 }
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
@@ -504,11 +526,36 @@ void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident: spins always progress
-  attr[0].val.cooperative = 1;
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for tcgen05 cta_group::2
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, tpf_fused_kernel, p);
+}
+
+// Largest number of co-resident CTA pairs (all CTAs must be resident: spins on
+// other CTAs' progress rely on it).
+int max_pairs() {
+  static int cached = -1;
+  if (cached >= 0) return cached;
+  cudaFuncSetAttribute(tpf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmemBytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, tpf_fused_kernel, &cfg) != cudaSuccess) n = 0;
+  cached = n;
+  return n;
 }
 
 }  // namespace tpf

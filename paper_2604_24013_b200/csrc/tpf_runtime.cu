@@ -37,6 +37,17 @@ constexpr int64_t kDefaultTimeoutNs = 10ll * 1000 * 1000 * 1000;
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Raster: m-block pairs that sweep the n-tiles together (L2 reuse of B). 16 pairs =
+// 32 m-blocks = 4096 rows: the 126 MB L2 holds that A panel plus the live B strips.
+int env_group_m() {
+  static int v = [] {
+    const char* e = std::getenv("TPF_GROUP_M");
+    const int x = (e && *e) ? std::atoi(e) : 16;
+    return x > 0 ? x : 16;
+  }();
+  return v;
+}
+
 int64_t env_timeout_ns() {
   const char* v = std::getenv("TPF_TIMEOUT_MS");
   if (v && *v) return static_cast<int64_t>(std::atoll(v)) * 1000 * 1000;
@@ -66,7 +77,8 @@ EncodeFn get_encode() {
 // bf16 tensor map with SWIZZLE_128B and zero OOB fill. dims/strides inner -> outer;
 // strides (bytes) for dims 1..rank-1.
 tpf::Status make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-                      const uint64_t* strides, const uint32_t* box) {
+                      const uint64_t* strides, const uint32_t* box,
+                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeFn enc = get_encode();
   if (!enc) return tpf::Status::cuda("cuTensorMapEncodeTiled unavailable (no CUDA driver)");
   if (reinterpret_cast<uintptr_t>(base) % 16)
@@ -84,7 +96,7 @@ tpf::Status make_tmap(CUtensorMap* m, const void* base, int rank, const uint64_t
     }
   }
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, s, b,
-                   e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   e, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return tpf::Status::cuda("cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
@@ -124,7 +136,7 @@ struct tpf_comm {
 namespace {
 
 struct Geometry {
-  int nmb_per_batch, nmb, nnt, nkb;
+  int nmb_per_batch, nmb, nnt, nkb, npairs;
   int64_t Sc;
 };
 
@@ -135,6 +147,7 @@ Geometry geometry(int64_t B, int64_t Sc, int64_t K, int64_t N) {
   g.nmb = static_cast<int>(B) * g.nmb_per_batch;
   g.nnt = static_cast<int>(ceil_div(N, tpf::BN));
   g.nkb = static_cast<int>(ceil_div(K, tpf::BK));
+  g.npairs = (g.nmb + 1) / 2;
   return g;
 }
 
@@ -191,6 +204,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.nmb = g.nmb;
   p.nnt = g.nnt;
   p.nkb = g.nkb;
+  p.npairs = g.npairs;
+  p.group_m = env_group_m();
   p.nsteps = k.T * k.m;
   p.B = static_cast<int>(k.B);
   p.Sc = k.Sc;
@@ -230,8 +245,21 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     p.flag_off[1] = kFlagBytesPerParity;
     p.data_off[0] = 2 * kFlagBytesPerParity;
     p.data_off[1] = 2 * kFlagBytesPerParity + data_cap;
+    p.parity = static_cast<int>((c->epoch + 1) & 1u);
     p.slot_bytes = slot_bytes;
     p.flags_per_slot = flags_per_slot;
+    if (k.op == tpf::OP_AG) {
+      // AG wire images of the hosted ranks' local slots: (128 B, 128 rows, image, slot, rank)
+      const int64_t rank_stride = R > 1 ? static_cast<int64_t>(c->sym_bytes) : nslots * slot_bytes;
+      const uint64_t dims[5] = {64, tpf::BM, static_cast<uint64_t>(g.nmb) * g.nkb,
+                                static_cast<uint64_t>(nslots), static_cast<uint64_t>(R)};
+      const uint64_t strides[4] = {128, tpf::kAStageBytes, static_cast<uint64_t>(slot_bytes),
+                                   static_cast<uint64_t>(rank_stride)};
+      const uint32_t box[5] = {64, tpf::BM, 1, 1, 1};
+      tpf::Status s = make_tmap(&p.tmap_wire, c->sym[k.rank0] + p.data_off[p.parity], 5, dims,
+                                strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+      if (!s.good()) return s;
+    }
     c->epoch += 1;
     p.epoch = c->epoch;
     p.parity = static_cast<int>(c->epoch & 1u);
@@ -246,9 +274,16 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
 
   const int sms = tpf::num_sms();
   if (sms <= 0) return tpf::Status::cuda("no CUDA device");
-  const int per_rank = std::max(1, sms / R);
-  p.ctas_per_rank = per_rank;
-  tpf::launch_fused(p, per_rank * R, stream);
+  int pairs = tpf::max_pairs();
+  if (pairs <= 0) return tpf::Status::cuda("kernel cannot be resident (cluster occupancy 0)");
+  pairs = std::min(pairs, sms / 2);
+  const int pairs_per_rank = pairs / R;
+  if (pairs_per_rank < 1)
+    return tpf::Status::invalid("local group of " + std::to_string(R) + " ranks needs " +
+                                std::to_string(R) + " resident CTA pairs, device has " +
+                                std::to_string(pairs));
+  p.ctas_per_rank = 2 * pairs_per_rank;
+  tpf::launch_fused(p, p.ctas_per_rank * R, stream);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return tpf::Status::cuda(std::string("kernel launch: ") + cudaGetErrorString(e));
   return tpf::Status::ok();
