@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 D_MODEL, FFN, SEQ = 4096, 14336, 8192
-WORKLOAD = "Llama-3-8B TP-SP MLP block (AG-GEMM gate||up -> SwiGLU -> GEMM-RS down), seq 8192"
+WORKLOAD = "Llama-3-8B TP-SP MLP block (AG-GEMM gate||up + fused SwiGLU -> GEMM-RS down), seq 8192"
 METRIC = "AG-GEMM/GEMM-RS TFLOP/s & exposed-comm us at TP=2/4/8; % of roofline"
 
 
@@ -169,33 +169,24 @@ def run_ours(args, rank, world, local_rank):
     S_l, F_l = SEQ // T, FFN // T
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn((1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
-    w_gu = (torch.randn((D_MODEL, 2 * F_l), device=dev, generator=g) / D_MODEL ** 0.5).to(torch.bfloat16)
+    w_gate = (torch.randn((D_MODEL, F_l), device=dev, generator=g) / D_MODEL ** 0.5).to(torch.bfloat16)
+    w_up = (torch.randn((D_MODEL, F_l), device=dev, generator=g) / D_MODEL ** 0.5).to(torch.bfloat16)
+    w_gu = tpf.interleave_gate_up(w_gate, w_up).contiguous()  # fused-SwiGLU shard layout
     w_dn = (torch.randn((F_l, D_MODEL), device=dev, generator=g) / FFN ** 0.5).to(torch.bfloat16)
-    hid = torch.empty((1, SEQ, 2 * F_l), device=dev, dtype=torch.bfloat16)
     act = torch.empty((1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
     y = torch.empty((1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
     stream = torch.cuda.current_stream(dev)
 
-    comm = None
-    if T > 1:
-        need = max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
-                   tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16))
-        comm = tpf.Communicator.from_process_group(need)
+    # T == 1 runs through the same communicator API (degenerate group: plain GEMMs).
+    need = max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
+               tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16))
+    comm = tpf.Communicator.from_process_group(need) if T > 1 else tpf.Communicator.create(0, 1, need)
 
-    def ag():
-        if comm is None:
-            tpf.gemm(x.view(S_l, D_MODEL), w_gu, hid.view(SEQ, 2 * F_l), stream=stream)
-        else:
-            comm.ag_gemm(x, w_gu, hid, stream=stream)
+    def ag(xin=x):
+        comm.ag_gemm(xin, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
 
-    def sw():
-        tpf.swiglu(hid, act, stream=stream)
-
-    def rs():
-        if comm is None:
-            tpf.gemm(act.view(SEQ, F_l), w_dn, y.view(S_l, D_MODEL), stream=stream)
-        else:
-            comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
+    def rs(yout=y):
+        comm.gemm_rs(act, w_dn, yout, kind=tpf.RING, wire=tpf.BF16, stream=stream)
 
     def barrier():
         if world > 1:
@@ -210,15 +201,14 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- warm-up
     for _ in range(args.warmup):
-        ag(); sw(); rs()
-    if comm:
-        comm.sync(stream)
+        ag(); rs()
+    comm.sync(stream)
     torch.cuda.synchronize(dev)
 
     # ---- timed region (device-resident inputs); per-kernel events on the launch stream
     sampler = ClockSampler(local_rank) if rank == 0 else None
     n = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
     barrier()
     torch.cuda.synchronize(dev)
     if sampler:
@@ -227,45 +217,73 @@ def run_ours(args, rank, world, local_rank):
         ev[i][0].record(stream)
         ag()
         ev[i][1].record(stream)
-        sw()
-        ev[i][2].record(stream)
         rs()
-        ev[i][3].record(stream)
+        ev[i][2].record(stream)
     torch.cuda.synchronize(dev)
     if sampler:
         sampler.mark_end()
     barrier()
-    if comm:
-        comm.sync(stream)
-    total_ms = ev[0][0].elapsed_time(ev[-1][3])
+    comm.sync(stream)
+    total_ms = ev[0][0].elapsed_time(ev[-1][2])
     ag_ms = sum(e[0].elapsed_time(e[1]) for e in ev) / n
-    sw_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / n
-    rs_ms = sum(e[2].elapsed_time(e[3]) for e in ev) / n
+    rs_ms = sum(e[1].elapsed_time(e[2]) for e in ev) / n
     ms_step = max_over_ranks(total_ms / n)
-    ag_ms, sw_ms, rs_ms = max_over_ranks(ag_ms), max_over_ranks(sw_ms), max_over_ranks(rs_ms)
+    ag_ms, rs_ms = max_over_ranks(ag_ms), max_over_ranks(rs_ms)
     clocks = sampler.stop() if sampler else None
     flops_step = block_flops(SEQ)  # whole job
     value = flops_step / (ms_step * 1e-3) / 1e12
 
-    # ---- e2e through the public API with pinned host buffers (copies timed)
-    x_host = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-    x_host.copy_(x.cpu())
-    y_host = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+    # ---- e2e through the public API with pinned host buffers (copies timed).
+    # Every step copies its input from pinned host memory and its result back; the copies
+    # run on their own streams (copy engines), double-buffered so step i+1's H2D and step
+    # i-1's D2H overlap step i's kernels.
+    nbuf = 2
+    x_host = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for _ in range(nbuf)]
+    y_host = [torch.empty(y.shape, dtype=y.dtype, pin_memory=True) for _ in range(nbuf)]
+    for hbuf in x_host:
+        hbuf.copy_(x.cpu())
+    x_dev = [torch.empty_like(x) for _ in range(nbuf)]
+    y_dev = [torch.empty_like(y) for _ in range(nbuf)]
+    s_in = torch.cuda.Stream(dev)
+    s_out = torch.cuda.Stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(n)]
+    ev_done = [torch.cuda.Event() for _ in range(n)]
+    ev_out = [torch.cuda.Event() for _ in range(n)]
+
+    def block(xin, yout):
+        ag(xin)
+        rs(yout)
+
     barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(n):
-        x.copy_(x_host, non_blocking=True)
-        ag(); sw(); rs()
-        y_host.copy_(y, non_blocking=True)
-    e1.record(stream)
+    e0.record(s_in)
+    stream.wait_stream(s_in)
+    s_out.wait_stream(s_in)
+    for i in range(n):
+        b = i % nbuf
+        with torch.cuda.stream(s_in):
+            if i >= nbuf:
+                s_in.wait_event(ev_done[i - nbuf])  # x_dev[b] consumed by step i-nbuf
+            x_dev[b].copy_(x_host[b], non_blocking=True)
+            ev_in[i].record(s_in)
+        stream.wait_event(ev_in[i])
+        if i >= nbuf:
+            stream.wait_event(ev_out[i - nbuf])  # y_dev[b] drained by step i-nbuf's D2H
+        block(x_dev[b], y_dev[b])
+        ev_done[i].record(stream)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_done[i])
+            y_host[b].copy_(y_dev[b], non_blocking=True)
+            ev_out[i].record(s_out)
+    s_out.wait_stream(stream)
+    e1.record(s_out)
     torch.cuda.synchronize(dev)
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n)
     e2e_value = flops_step / (e2e_ms * 1e-3) / 1e12
-    h2d = x_host.numel() * x_host.element_size() * world
-    d2h = y_host.numel() * y_host.element_size() * world
+    h2d = x_host[0].numel() * x_host[0].element_size() * world
+    d2h = y_host[0].numel() * y_host[0].element_size() * world
 
     # ---- non-overlapped baseline: cuBLAS (+ NCCL all-gather / reduce-scatter for T > 1)
     base_ms = None
@@ -278,8 +296,8 @@ def run_ours(args, rank, world, local_rank):
                 dist.all_gather_into_tensor(xg, x)
             else:
                 xg.copy_(x)
-            h = torch.matmul(xg.view(SEQ, D_MODEL), w_gu)
-            gt, up = h.chunk(2, dim=-1)
+            gt = torch.matmul(xg.view(SEQ, D_MODEL), w_gate)
+            up = torch.matmul(xg.view(SEQ, D_MODEL), w_up)
             a = torch.nn.functional.silu(gt) * up
             torch.matmul(a, w_dn, out=yfull.view(SEQ, D_MODEL))
             if T > 1:
@@ -340,21 +358,23 @@ def run_ours(args, rank, world, local_rank):
                    "ffn": FFN, "parallelism": f"tp{T}-sp" if T > 1 else "tp1 (degenerate: plain GEMMs)",
                    "rs_schedule": "ring", "rs_wire": "bf16",
                    "l2": "no flush: per-step working set ~1.0 GB (weights 352 MB + hidden 470 MB) > 126 MB L2"},
-        "gpu_launches": 3 * n,
+        "gpu_launches": 2 * n,
         "ops": {
-            "ag_gemm": {"ms": ag_ms, "tflops": 2.0 * SEQ * D_MODEL * 2 * FFN / (ag_ms * 1e-3) / 1e12},
-            "swiglu": {"ms": sw_ms, "gbs": 3.0 * SEQ * F_l * 2 * T / (sw_ms * 1e-3) / 1e9},
+            "ag_gemm_swiglu": {"ms": ag_ms, "tflops": 2.0 * SEQ * D_MODEL * 2 * FFN / (ag_ms * 1e-3) / 1e12,
+                               "note": "AG-GEMM gate||up with SwiGLU fused in the epilogue"},
             "gemm_rs": {"ms": rs_ms, "tflops": 2.0 * SEQ * FFN * D_MODEL / (rs_ms * 1e-3) / 1e12},
             "exposed_comm_us": 0.0 if T == 1 else None,
         },
-        "roofline": {"kernel": "tpf_fused_kernel (AG-GEMM gate||up)", "bound": "tensor",
+        "roofline": {"kernel": "tpf_fused_kernel (AG-GEMM gate||up + fused SwiGLU)", "bound": "tensor",
                      "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
                      "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
                      "peak_src": f"{pk['src']} burst; frac vs sustained {pk['bf16_tflops_sustained']}: "
                                  f"{achieved / pk['bf16_tflops_sustained']:.3f}",
                      "flops_per_launch": ag_flops},
         "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms},
+                "ms_per_step": e2e_ms, "gpu_launches": 2 * n,
+                "how": "C-ABI calls; pinned host x -> device and y -> host every step, copies on "
+                       "separate streams double-buffered against the kernels"},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
@@ -378,34 +398,30 @@ def emulated_block(args, dev, stream, T):
     x = torch.randn((T, 1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
     w_gu = (torch.randn((T, D_MODEL, 2 * F_l), device=dev, generator=g) / 64).to(torch.bfloat16)
     w_dn = (torch.randn((T, F_l, D_MODEL), device=dev, generator=g) / 120).to(torch.bfloat16)
-    hid = torch.empty((T, 1, SEQ, 2 * F_l), device=dev, dtype=torch.bfloat16)
     act = torch.empty((T, 1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
     y = torch.empty((T, 1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
     comm = tpf.Communicator.local_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
                                                tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
 
     def step():
-        comm.ag_gemm(x, w_gu, hid, stream=stream)
-        tpf.swiglu(hid, act, stream=stream)
+        comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
         comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
 
     for _ in range(args.warmup):
         step()
     comm.sync(stream)
     n = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(n)]
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
     for i in range(n):
         ev[i][0].record(stream)
-        comm.ag_gemm(x, w_gu, hid, stream=stream)
+        comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
         ev[i][1].record(stream)
-        tpf.swiglu(hid, act, stream=stream)
-        ev[i][2].record(stream)
         comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
-        ev[i][3].record(stream)
+        ev[i][2].record(stream)
     comm.sync(stream)
-    total = ev[0][0].elapsed_time(ev[-1][3]) / n
+    total = ev[0][0].elapsed_time(ev[-1][2]) / n
     ag = sum(e[0].elapsed_time(e[1]) for e in ev) / n
-    rs = sum(e[2].elapsed_time(e[3]) for e in ev) / n
+    rs = sum(e[1].elapsed_time(e[2]) for e in ev) / n
     comm.close()
     return {"tp": T, "note": "all ranks on ONE GPU (local group); wire traffic goes through local HBM, not NVLink",
             "ms_per_step": total, "tflops": block_flops(SEQ) / (total * 1e-3) / 1e12,

@@ -45,6 +45,11 @@ extern "C" {
  * layers.hpp:58; only the exactly-representable ones run fused). */
 #define TPF_ACT_NONE 0
 #define TPF_ACT_SQUARE 1
+/* Llama SwiGLU fused into the AG-GEMM epilogue: w is the tile-interleaved
+ * gate||up shard — for every 256-column tile t, columns [256t, 256t+128) are
+ * gate columns [128t, 128t+128) and [256t+128, 256t+256) the matching up
+ * columns (N_local % 256 == 0). out is (B, S, N_local/2) = silu(gate) * up. */
+#define TPF_ACT_SWIGLU 2
 
 typedef struct tpf_comm tpf_comm;
 

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libtpfuse_b200.so")
 RING, PAIRWISE, CIRCULAR = 0, 1, 2
 KIND_NAMES = {RING: "ring", PAIRWISE: "pairwise", CIRCULAR: "circular-slices"}
 BF16, F32 = 0, 1
-ACT_NONE, ACT_SQUARE = 0, 1
+ACT_NONE, ACT_SQUARE, ACT_SWIGLU = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 
 # include/tpf.h error codes -> reference exception types (SURVEY §8(b) Errors)
@@ -227,6 +227,18 @@ class Communicator:
         N = w.shape[-1]
         _check(_lib.tpf_gemm_rs(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B, S, K, N,
                                 kind, m, wire, _dtype_code(out), _stream_ptr(stream)))
+
+
+def interleave_gate_up(gate, up, tile: int = 256):
+    """Tile-interleaved gate||up shard for the fused SwiGLU epilogue (ACT_SWIGLU):
+    every 256-column tile holds 128 gate columns followed by the matching 128 up
+    columns. gate, up: (K, F) with F % 128 == 0 -> (K, 2F)."""
+    import torch
+    K, F = gate.shape
+    half = tile // 2
+    assert up.shape == gate.shape and F % half == 0
+    return torch.stack([gate.reshape(K, F // half, half), up.reshape(K, F // half, half)],
+                       dim=2).reshape(K, 2 * F)
 
 
 def _dtype_code(t) -> int:

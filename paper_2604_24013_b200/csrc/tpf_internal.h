@@ -19,7 +19,7 @@ constexpr int kStageBytes = kAStageBytes + kBStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
-enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1 };
+enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };
 
 // Error record in device memory (first error wins).
 //   [0] code (0 ok, 1 peer-flag timeout, 2 mbarrier timeout)

@@ -422,17 +422,35 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows +
                              (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
         char* rp = out_h + orow * p.N * esz;
-        for (int j = 0; j < BN / 32; ++j) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(taddr + j * 32, r);
-          tmem_ld_wait();
-          float v[32];
+        if (p.act == ACT_SWIGLU) {
+          // Tile-interleaved W: columns [0,128) of the tile are gate, [128,256) the matching
+          // up columns -> 128 output columns silu(gate) * up (Llama MLP, fused).
+          for (int j = 0; j < BN / 64; ++j) {
+            uint32_t rg[32], ru[32];
+            tmem_ld_32x32b_x32(taddr + j * 32, rg);
+            tmem_ld_32x32b_x32(taddr + BN / 2 + j * 32, ru);
+            tmem_ld_wait();
+            float v[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float x = __uint_as_float(r[c]);
-            v[c] = p.act == ACT_SQUARE ? x * x : x;
+            for (int c = 0; c < 32; ++c) {
+              const float gt = __uint_as_float(rg[c]);
+              v[c] = __fdividef(gt, 1.0f + __expf(-gt)) * __uint_as_float(ru[c]);
+            }
+            if (valid) store_out_row(p, rp, static_cast<int64_t>(t.nt) * (BN / 2) + j * 32, v);
           }
-          if (valid) store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
+        } else {
+          for (int j = 0; j < BN / 32; ++j) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(taddr + j * 32, r);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+              const float x = __uint_as_float(r[c]);
+              v[c] = p.act == ACT_SQUARE ? x * x : x;
+            }
+            if (valid) store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
+          }
         }
         tc_fence_before();
         __syncwarp();

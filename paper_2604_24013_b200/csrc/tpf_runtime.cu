@@ -158,6 +158,7 @@ int64_t data_bytes_per_parity(size_t sym_bytes) {
 struct Call {
   int op, T, m, direct, act, wire_f32, out_f32, n_hosted, rank0;
   int64_t B, Sc, K, N, x_rows, out_rows;
+  int64_t N_gemm;  // columns of W (B operand); == N unless the epilogue narrows (SwiGLU)
   const void* x;
   const void* w;
   void* out;
@@ -167,10 +168,11 @@ struct Call {
 tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   tpf::KParams p;
   std::memset(&p, 0, sizeof(p));
-  const Geometry g = geometry(k.B, k.Sc, k.K, k.N);
+  const int64_t NG = k.N_gemm > 0 ? k.N_gemm : k.N;
+  const Geometry g = geometry(k.B, k.Sc, k.K, NG);
   const int R = k.n_hosted;
   const int64_t x_rank_stride = k.B * k.x_rows * k.K * 2;
-  const int64_t w_rank_stride = k.K * k.N * 2;
+  const int64_t w_rank_stride = k.K * NG * 2;
   const int64_t esz = k.out_f32 ? 4 : 2;
   {
     const uint64_t dims[4] = {static_cast<uint64_t>(k.K), static_cast<uint64_t>(k.x_rows),
@@ -183,9 +185,9 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     if (!s.good()) return s;
   }
   {
-    const uint64_t dims[3] = {static_cast<uint64_t>(k.N), static_cast<uint64_t>(k.K),
+    const uint64_t dims[3] = {static_cast<uint64_t>(NG), static_cast<uint64_t>(k.K),
                               static_cast<uint64_t>(R)};
-    const uint64_t strides[2] = {static_cast<uint64_t>(k.N * 2),
+    const uint64_t strides[2] = {static_cast<uint64_t>(NG * 2),
                                  static_cast<uint64_t>(w_rank_stride)};
     const uint32_t box[3] = {64, tpf::BK, 1};
     tpf::Status s = make_tmap(&p.tmap_b, k.w, 3, dims, strides, box);
@@ -510,6 +512,11 @@ int tpf_ag_gemm(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
                                      " is not divisible by granularity " + std::to_string(m)));
   if (K % 8 || N_local % 8)
     return fail(tpf::Status::shape("column_parallel_forward: K and N_local must be multiples of 8"));
+  if (act < TPF_ACT_NONE || act > TPF_ACT_SWIGLU)
+    return fail(tpf::Status::invalid("column_parallel_forward: unknown activation"));
+  if (act == TPF_ACT_SWIGLU && N_local % tpf::BN)
+    return fail(tpf::Status::shape("SwiGLU epilogue needs the tile-interleaved gate||up shard with "
+                                   "N_local a multiple of 256"));
   std::vector<int32_t> sched;
   Call k{};
   k.op = tpf::OP_AG;
@@ -519,7 +526,9 @@ int tpf_ag_gemm(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
   k.out_f32 = out_dtype == TPF_F32;
   k.n_hosted = hosted(c);
   k.rank0 = c->local_group ? 0 : c->rank;
-  k.B = B; k.Sc = T > 1 ? sl / m : S; k.K = K; k.N = N_local; k.x_rows = sl; k.out_rows = S;
+  k.B = B; k.Sc = T > 1 ? sl / m : S; k.K = K; k.x_rows = sl; k.out_rows = S;
+  k.N_gemm = N_local;
+  k.N = act == TPF_ACT_SWIGLU ? N_local / 2 : N_local;
   k.x = x; k.w = w; k.out = out;
   if (T > 1) {
     sched.resize(static_cast<size_t>(T) * T * 3);

@@ -379,3 +379,29 @@ def test_swiglu_matches_torch():
     g, u = gu.float().chunk(2, dim=-1)
     ref = torch.nn.functional.silu(g) * u
     assert (out.float() - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("T", [1, 2, 8])
+def test_ag_gemm_fused_swiglu(T):
+    """Llama MLP up-projection with SwiGLU fused into the AG-GEMM epilogue
+    (tile-interleaved gate||up shard) vs an fp32 torch reference."""
+    B, S, K, F = 1, 256 * T, 512, 256 * T
+    g = torch.Generator(device=DEV).manual_seed(T)
+    x = torch.randn((T, B, S // T, K), device=DEV, generator=g).to(torch.bfloat16)
+    gate = (torch.randn((K, F), device=DEV, generator=g) / K ** 0.5).to(torch.bfloat16)
+    up = (torch.randn((K, F), device=DEV, generator=g) / K ** 0.5).to(torch.bfloat16)
+    fl = F // T
+    w = torch.stack([tpf.interleave_gate_up(gate[:, r * fl:(r + 1) * fl], up[:, r * fl:(r + 1) * fl])
+                     for r in range(T)]).contiguous()
+    out = torch.empty((T, B, S, fl), device=DEV, dtype=torch.float32)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, B, S, K, 2 * fl, 1))
+    comm.ag_gemm(x, w, out, act=tpf.ACT_SWIGLU)
+    comm.sync()
+    comm.close()
+    xg = x.reshape(B * S, K).float()
+    for r in range(T):
+        gg = xg @ gate[:, r * fl:(r + 1) * fl].float()
+        uu = xg @ up[:, r * fl:(r + 1) * fl].float()
+        ref = torch.nn.functional.silu(gg) * uu
+        err = (out[r].reshape(B * S, fl) - ref).abs().max().item()
+        assert err <= 1e-3 * ref.abs().max().item() + 1e-5, (r, err)
