@@ -105,6 +105,10 @@ int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns);
  * had failed mid-collective; its successors time out and tpf_comm_sync reports
  * TPF_E_PEER naming the waiting rank. */
 int tpf_comm_inject_fault(tpf_comm* c, int rank);
+/* Measurement hook: on != 0 runs the same kernels over the same tile schedule with
+ * every peer flag wait, wire store/load and ring forward disabled (results are
+ * NOT the collective's). exposed comm = t(fused) - t(compute-only), SURVEY 8(d). */
+int tpf_comm_set_compute_only(tpf_comm* c, int on);
 
 /* -------------------------------------------------------------- fused ops
  * AG-GEMM. Replaces:

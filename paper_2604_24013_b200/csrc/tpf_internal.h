@@ -66,6 +66,7 @@ struct KParams {
   uint32_t* err;
   int64_t timeout_ns;
   int fault_rank;   // test hook: this rank never publishes its flags (-1: none)
+  int compute_only; // measurement: same tiles, no flag waits / wire traffic (exposed-comm baseline)
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);

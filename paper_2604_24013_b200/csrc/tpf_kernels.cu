@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       for (int lin = gp; lin < ntiles; lin += GP) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
-        const bool a_from_wire = (p.op == OP_AG) && it > 0;
+        const bool a_from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
         int64_t arow;
         if (t.valid == 0)
           arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     }
   } else if (warp == 2 || warp == 3) {
     // ===================================================== AG ring forwarding
-    if (p.op == OP_AG && p.T > 1) {
+    if (p.op == OP_AG && p.T > 1 && !p.compute_only) {
       const int cw = warp - 2;
       const int per_slot = p.nmb * p.nkb;
       const int npieces = p.m * (p.T - 1) * per_slot;
@@ -459,16 +459,16 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       }
 
       // ------------------------------------------------ OP_RS
-      const bool last = (it == p.T - 1);
+      const bool last = (it == p.T - 1) || p.compute_only;
       const int slot_send = pass * (p.T - 1) + it;
       const int send_rank = p.T > 1 ? p.sched[rank][it][0] : -1;
       const char* inbox = nullptr;
-      if (tile_live && !p.direct && it > 0) {
+      if (tile_live && !p.direct && it > 0 && !p.compute_only) {
         const int slot_in = slot_send - 1;
         wait_flag(p, flag_ptr(p, rank, slot_in, fidx), rank, t.step, lin);
         inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
       }
-      if (tile_live && p.direct && last && p.T > 1) {
+      if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
         for (int s = 0; s < p.T - 1; ++s)
           wait_flag(p, flag_ptr(p, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin);
       }
@@ -491,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             wire_load(p.wire_f32, inbox, j, row, in);
 #pragma unroll
             for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
-          } else if (p.direct && last && p.T > 1) {
+          } else if (p.direct && last && p.T > 1 && !p.compute_only) {
             // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
             float acc[32];
             wire_load(p.wire_f32, slot_ptr(p, rank, pass * (p.T - 1)) + tile_idx * tile_bytes, j,

@@ -131,6 +131,7 @@ struct tpf_comm {
   int64_t timeout_ns = kDefaultTimeoutNs;
   int device = 0;
   int fault_rank = -1;
+  int compute_only = 0;
 };
 
 namespace {
@@ -221,6 +222,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.out_rank_stride = k.B * k.out_rows * k.N * esz;
   p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
   p.fault_rank = c ? c->fault_rank : -1;
+  p.compute_only = c ? c->compute_only : 0;
   if (k.T > 1) {
     for (int r = 0; r < k.T; ++r)
       for (int i = 0; i < k.T; ++i)
@@ -438,6 +440,12 @@ int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
   c->timeout_ns = ns > 0 ? ns : env_timeout_ns();
+  return TPF_OK;
+}
+
+int tpf_comm_set_compute_only(tpf_comm* c, int on) {
+  if (!c) return fail(tpf::Status::invalid("null communicator"));
+  c->compute_only = on ? 1 : 0;
   return TPF_OK;
 }
 
