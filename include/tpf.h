@@ -109,6 +109,13 @@ int tpf_comm_inject_fault(tpf_comm* c, int rank);
  * every peer flag wait, wire store/load and ring forward disabled (results are
  * NOT the collective's). exposed comm = t(fused) - t(compute-only), SURVEY 8(d). */
 int tpf_comm_set_compute_only(tpf_comm* c, int on);
+/* Device timeline trace: buffer = device memory of (capacity+1) * 32
+ * bytes, zeroed by the caller; word 0 counts records, record k (k >= 1) is
+ * {kind | rank<<8 | block<<16 | step<<32, index, t0_ns, t1_ns} (%globaltimer).
+ * Kinds: 1 tile epilogue, 2 producer main loop, 3 AG piece forwarded, 4 producer
+ * wait on an AG wire image, 5 epilogue wait on an RS inbox, 6 RS flag published.
+ * NULL disables (default). Used for the measured no-tail check. */
+int tpf_comm_set_trace(tpf_comm* c, void* buffer, int64_t capacity_records);
 
 /* -------------------------------------------------------------- fused ops
  * AG-GEMM. Replaces:

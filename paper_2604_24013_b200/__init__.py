@@ -68,6 +68,7 @@ _lib.tpf_comm_sync.argtypes = [_vp, _vp]
 _lib.tpf_comm_set_timeout_ns.argtypes = [_vp, _i64]
 _lib.tpf_comm_inject_fault.argtypes = [_vp, C.c_int]
 _lib.tpf_comm_set_compute_only.argtypes = [_vp, C.c_int]
+_lib.tpf_comm_set_trace.argtypes = [_vp, _vp, _i64]
 _lib.tpf_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 3 + [_vp]
 _lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + [_vp]
 _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
@@ -81,7 +82,7 @@ EXPORTED_SYMBOLS = (
     "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
     "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
     "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", ""tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
     "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
 )
 
@@ -195,6 +196,13 @@ class Communicator:
     def set_compute_only(self, on: bool) -> None:
         """Measurement hook: same kernels, no flag waits / wire traffic (exposed-comm baseline)."""
         _check(_lib.tpf_comm_set_compute_only(self._h, int(bool(on))))
+
+    def set_trace(self, buf) -> None:
+        """Attach a zeroed device int64 tensor of (cap+1)*4 words as the timeline trace (None: off)."""
+        if buf is None:
+            _check(_lib.tpf_comm_set_trace(self._h, None, 0))
+        else:
+            _check(_lib.tpf_comm_set_trace(self._h, buf.data_ptr(), buf.numel() // 4 - 1))
 
     def sync(self, stream=None) -> None:
         """Synchronise the stream and raise GroupError if a peer wait timed out."""

@@ -67,6 +67,19 @@ struct KParams {
   int64_t timeout_ns;
   int fault_rank;   // test hook: this rank never publishes its flags (-1: none)
   int compute_only; // measurement: same tiles, no flag waits / wire traffic (exposed-comm baseline)
+  // Optional device trace (%globaltimer ns): records of 4 x u64 appended via trace[0] counter.
+  unsigned long long* trace;
+  int64_t trace_cap;  // records
+};
+
+// trace record: {kind | rank << 8 | cta(block) << 16 | step << 32, index, t0, t1}
+enum TraceKind : int {
+  TR_TILE = 1,       // index = tile lin; t0 = accumulator ready (epilogue start), t1 = epilogue done
+  TR_MAINLOOP = 2,   // index = tile lin; t0 = first stage issued, t1 = last stage issued (producer)
+  TR_AG_PIECE = 3,   // index = piece;   t0 = source ready, t1 = flag published
+  TR_WAIT_A = 4,     // index = tile lin*1024+kb; producer blocked on an AG wire image (t1-t0)
+  TR_WAIT_IN = 5,    // index = tile lin; epilogue blocked on an RS inbox flag
+  TR_FLAG = 6,       // index = tile lin; RS flag published to the successor at t1
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);

@@ -63,6 +63,20 @@ __device__ __forceinline__ Tile get_tile(const KParams& p, int lin, int cta) {
   return t;
 }
 
+__device__ __forceinline__ void trace_rec(const KParams& p, int kind, int rank, int step,
+                                          int64_t index, uint64_t t0, uint64_t t1) {
+  if (!p.trace) return;
+  const unsigned long long slot = atomicAdd(p.trace, 1ull);
+  if (static_cast<int64_t>(slot) >= p.trace_cap) return;
+  unsigned long long* r = p.trace + 4 * (slot + 1);
+  r[0] = static_cast<unsigned long long>(kind) | (static_cast<unsigned long long>(rank & 0xFF) << 8) |
+         (static_cast<unsigned long long>(blockIdx.x & 0xFFFF) << 16) |
+         (static_cast<unsigned long long>(static_cast<uint32_t>(step)) << 32);
+  r[1] = static_cast<unsigned long long>(index);
+  r[2] = t0;
+  r[3] = t1;
+}
+
 __device__ __forceinline__ bool aborted(const KParams& p) {
   return ld_relaxed_sys(p.err + 4) != 0;
 }
@@ -194,12 +208,67 @@ __device__ __forceinline__ void wire_load(int wire_f32, const char* tile, int j,
   }
 }
 
+// rs_direct fold of one 32-column sub-chunk, 16 columns at a time: all T-1 received
+// contributions are loaded first (memory-level parallelism), then summed in the
+// reference order ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own.
+__device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0, int j, int row,
+                                            float (&v)[32]) {
+  const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
+  const int64_t slot_stride = p.slot_bytes;
+  const int nin = p.T - 1;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint4 raw[kMaxRanks - 1][4];
+#pragma unroll
+    for (int s = 0; s < kMaxRanks - 1; ++s) {
+      if (s < nin) {
+        const char* tile = slot0 + s * slot_stride;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (p.wire_f32) {
+            raw[s][q] = *reinterpret_cast<const uint4*>(tile + wire_off(1, j, half * 4 + q, row));
+          } else if (q < 2) {
+            raw[s][q] = *reinterpret_cast<const uint4*>(tile + wire_off(0, j, half * 2 + q, row));
+          }
+        }
+      }
+    }
+    float acc[16];
+#pragma unroll
+    for (int s = 0; s < kMaxRanks - 1; ++s) {
+      if (s < nin) {
+        float in[16];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (p.wire_f32) {
+            in[q * 4 + 0] = __uint_as_float(raw[s][q].x);
+            in[q * 4 + 1] = __uint_as_float(raw[s][q].y);
+            in[q * 4 + 2] = __uint_as_float(raw[s][q].z);
+            in[q * 4 + 3] = __uint_as_float(raw[s][q].w);
+          } else if (q < 2) {
+            in[q * 8 + 0] = bf16lo(raw[s][q].x); in[q * 8 + 1] = bf16hi(raw[s][q].x);
+            in[q * 8 + 2] = bf16lo(raw[s][q].y); in[q * 8 + 3] = bf16hi(raw[s][q].y);
+            in[q * 8 + 4] = bf16lo(raw[s][q].z); in[q * 8 + 5] = bf16hi(raw[s][q].z);
+            in[q * 8 + 6] = bf16lo(raw[s][q].w); in[q * 8 + 7] = bf16hi(raw[s][q].w);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) acc[c] = s == 0 ? in[c] : acc[c] + in[c];
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[half * 16 + c] = acc[c] + v[half * 16 + c];
+  }
+  (void)tile_bytes;
+}
+
 // -------------------------------------------------------------- AG forwarding
 // One warp moves one 16 KiB piece (m-block mb, k-block kb) of the travelling chunk to
 // the ring successor. Hop 0 reads this rank's x (row-major) and writes the SWIZZLE_128B
 // operand image; later hops copy the received image verbatim.
 __device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, int mb, int kb,
                                  int lane) {
+  uint64_t t_src = p.trace ? globaltimer() : 0;
   const int T = p.T;
   const int pass = slot / (T - 1);
   const int it = slot - pass * (T - 1);
@@ -234,6 +303,7 @@ __device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, in
     const uint32_t* f = flag_ptr(p, rank, slot - 1, static_cast<int64_t>(mb) * p.nkb + kb);
     wait_flag(p, f, rank, slot, mb * p.nkb + kb);
     __syncwarp();
+    if (p.trace) t_src = globaltimer();
     const char* src =
         slot_ptr(p, rank, slot - 1) + (static_cast<int64_t>(mb) * p.nkb + kb) * kAStageBytes;
 #pragma unroll 1
@@ -251,6 +321,7 @@ __device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, in
   __syncwarp();
   if (lane == 0 && rank != p.fault_rank)
     st_release_sys(flag_ptr(p, dst_rank, slot, static_cast<int64_t>(mb) * p.nkb + kb), p.epoch);
+  if (lane == 0 && p.trace) trace_rec(p, TR_AG_PIECE, rank, slot, static_cast<int64_t>(mb) * p.nkb + kb, t_src, globaltimer());
 }
 
 }  // namespace
@@ -321,14 +392,28 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         else
           arow = pass * p.Sc + t.row0;
         const int aslot = pass * (p.T - 1) + it - 1;
+        int ready = -1;  // wire images [0, ready] of this m-block are known to have landed
+        uint64_t t_first = 0;
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(p, empty + stage, phase ^ 1);
           uint8_t* sa = smem_a + stage * kAStageBytes;
           uint8_t* sb = smem_b + stage * kBStageBytes;
           const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
           const int img = t.mb * p.nkb + kb;
-          if (a_from_wire && t.valid) {
-            wait_flag(p, flag_ptr(p, rank, aslot, img), rank, t.step, lin);
+          if (a_from_wire && t.valid && kb > ready) {
+            // Wait for this image, then claim every consecutive image that has already
+            // landed (relaxed reads of adjacent flag words); one system-scope fence +
+            // proxy fence then orders all of them before the TMA reads.
+            const uint32_t* f = flag_ptr(p, rank, aslot, static_cast<int64_t>(t.mb) * p.nkb);
+            const uint64_t tw0 = p.trace ? globaltimer() : 0;
+            wait_flag(p, f + kb, rank, t.step, lin);
+            if (p.trace) {
+              const uint64_t tw1 = globaltimer();
+              if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
+            }
+            ready = kb;
+            while (ready + 1 < p.nkb && ld_relaxed_sys(f + ready + 1) >= p.epoch) ++ready;
+            fence_sys();
             fence_proxy_async_global();
           }
           if (leader)
@@ -343,8 +428,10 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           for (int q = 0; q < BN / 128; ++q)
             tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                             kb * BK, h);
+          if (p.trace && kb == 0) t_first = globaltimer();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+        if (p.trace) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
       }
     }
   } else if (warp == 1) {
@@ -410,6 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
       mbar_wait(p, tfull + a, use & 1);
       tc_fence_after();
+      const uint64_t t_epi0 = (p.trace && lane == 0) ? globaltimer() : 0;
       const int pass = t.step / p.T, it = t.step - pass * p.T;
       const bool valid = row < t.valid;
       const bool tile_live = t.valid > 0;
@@ -455,6 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
+        if (p.trace && lane == 0 && ew == 0 && tile_live)
+          trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());
         continue;
       }
 
@@ -465,7 +555,12 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const char* inbox = nullptr;
       if (tile_live && !p.direct && it > 0 && !p.compute_only) {
         const int slot_in = slot_send - 1;
+        const uint64_t tw0 = (p.trace && lane == 0) ? globaltimer() : 0;
         wait_flag(p, flag_ptr(p, rank, slot_in, fidx), rank, t.step, lin);
+        if (p.trace && lane == 0 && ew == 0) {
+          const uint64_t tw1 = globaltimer();
+          if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_IN, rank, t.step, lin, tw0, tw1);
+        }
         inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
       }
       if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
@@ -493,19 +588,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
           } else if (p.direct && last && p.T > 1 && !p.compute_only) {
             // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
-            float acc[32];
-            wire_load(p.wire_f32, slot_ptr(p, rank, pass * (p.T - 1)) + tile_idx * tile_bytes, j,
-                      row, acc);
-            for (int s = 1; s < p.T - 1; ++s) {
-              float in[32];
-              wire_load(p.wire_f32,
-                        slot_ptr(p, rank, pass * (p.T - 1) + s) + tile_idx * tile_bytes, j, row,
-                        in);
-#pragma unroll
-              for (int c = 0; c < 32; ++c) acc[c] = acc[c] + in[c];
-            }
-#pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = acc[c] + v[c];
+            const char* in0 = slot_ptr(p, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
+            direct_fold(p, in0, j, row, v);
           }
           if (last)
             store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
@@ -521,7 +605,10 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         __syncwarp();
         if (lane == 0 && rank != p.fault_rank)
           st_release_sys(flag_ptr(p, send_rank, slot_send, fidx), p.epoch);
+        if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_FLAG, rank, t.step, lin, t_epi0, globaltimer());
       }
+      if (p.trace && lane == 0 && ew == 0 && tile_live)
+        trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());
     }
   }
 

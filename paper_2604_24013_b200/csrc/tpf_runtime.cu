@@ -132,6 +132,8 @@ struct tpf_comm {
   int device = 0;
   int fault_rank = -1;
   int compute_only = 0;
+  unsigned long long* trace = nullptr;
+  int64_t trace_cap = 0;
 };
 
 namespace {
@@ -223,6 +225,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
   p.fault_rank = c ? c->fault_rank : -1;
   p.compute_only = c ? c->compute_only : 0;
+  p.trace = c ? c->trace : nullptr;
+  p.trace_cap = c ? c->trace_cap : 0;
   if (k.T > 1) {
     for (int r = 0; r < k.T; ++r)
       for (int i = 0; i < k.T; ++i)
@@ -440,6 +444,13 @@ int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
   c->timeout_ns = ns > 0 ? ns : env_timeout_ns();
+  return TPF_OK;
+}
+
+int tpf_comm_set_trace(tpf_comm* c, void* buffer, int64_t capacity_records) {
+  if (!c) return fail(tpf::Status::invalid("null communicator"));
+  c->trace = static_cast<unsigned long long*>(buffer);
+  c->trace_cap = buffer ? capacity_records : 0;
   return TPF_OK;
 }
 
