@@ -82,7 +82,7 @@ EXPORTED_SYMBOLS = (
     "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
     "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
     "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", ""tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
     "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
 )
 
