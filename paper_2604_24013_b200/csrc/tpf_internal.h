@@ -16,7 +16,7 @@ constexpr int kThreads = 256;    // 8 warps: TMA, MMA, 2x comm, 4x epilogue
 constexpr int kAStageBytes = BM * BK * 2;        // 16 KiB: also the AG wire "image" unit
 constexpr int kBStageBytes = (BN / 2) * BK * 2;  // 16 KiB: this CTA's half of B
 constexpr int kStageBytes = kAStageBytes + kBStageBytes;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 256;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 512;  // + barriers
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
 enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };
@@ -38,6 +38,8 @@ struct KParams {
   int rank0;           // rank id of hosted rank 0
   int ctas_per_rank;   // CTAs serving one hosted rank (even: CTA pairs)
   int group_m;         // raster: m-block pairs that sweep the n-tiles together
+  int ag_nfwd;         // AG: leading n-tiles of an m-block that forward its images
+  int ag_batch;        // AG: forwards per fence + flag publication (<= 16)
   int act;             // AG epilogue activation (Act)
   int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
   int out_f32;         // output dtype: 1 fp32, 0 bf16
@@ -80,6 +82,7 @@ enum TraceKind : int {
   TR_WAIT_A = 4,     // index = tile lin*1024+kb; producer blocked on an AG wire image (t1-t0)
   TR_WAIT_IN = 5,    // index = tile lin; epilogue blocked on an RS inbox flag
   TR_FLAG = 6,       // index = tile lin; RS flag published to the successor at t1
+  TR_FLUSH = 7,      // index = #flags; AG forwarder fence + flag publication (t1-t0)
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);

@@ -12,7 +12,8 @@
 //               full barrier
 //   warp 1      (leader CTA only) tcgen05.mma.cta_group::2, 256x256x16 bf16 -> fp32, two
 //               TMEM accumulators; commits multicast to both CTAs' barriers
-//   warps 2-3   TMEM allocator / AG ring-forwarding comm warps (NVLink peer stores)
+//   warp 2      TMEM allocator; AG ring forwarder: bulk-stores each landed A stage (already
+//               the SWIZZLE_128B operand image) from SMEM to the successor's slot over NVLink
 //   warps 4-7   epilogue: tcgen05.ld of this CTA's 128 rows -> (+ inbox) -> peer / output
 //
 // Work is a static, iteration-major tile list (step = pass * T + iteration), so every
@@ -20,8 +21,9 @@
 // progress. Wire formats are chosen so the consumer does no re-layout:
 //   RS wire  = the TMEM 32x32b fragment image (thread-row interleaved by 16 B column
 //              groups), so each warp-wide 16 B store/load touches 512 contiguous bytes;
-//   AG wire  = the SWIZZLE_128B K-major UMMA operand image of a 128x64 A tile (16 KiB),
-//              so the receiver bulk-copies it straight into a pipeline stage.
+//   AG wire  = the SWIZZLE_128B K-major UMMA operand image of a 128x64 A tile (16 KiB):
+//              exactly the bytes of the sender's pipeline stage, so forwarding is one
+//              SMEM->peer bulk store and the receiver TMA-loads it straight into a stage.
 // Flags carry the per-call epoch (monotonic, never reset); slots are double-buffered by
 // epoch parity. Every spin is bounded by a %globaltimer deadline and reports into a
 // device error record instead of trapping.
@@ -262,68 +264,6 @@ __device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0,
   (void)tile_bytes;
 }
 
-// -------------------------------------------------------------- AG forwarding
-// One warp moves one 16 KiB piece (m-block mb, k-block kb) of the travelling chunk to
-// the ring successor. Hop 0 reads this rank's x (row-major) and writes the SWIZZLE_128B
-// operand image; later hops copy the received image verbatim.
-__device__ void ag_forward_piece(const KParams& p, int h, int rank, int slot, int mb, int kb,
-                                 int lane) {
-  uint64_t t_src = p.trace ? globaltimer() : 0;
-  const int T = p.T;
-  const int pass = slot / (T - 1);
-  const int it = slot - pass * (T - 1);
-  const int dst_rank = p.sched[rank][it][0];
-  char* dst = slot_ptr(p, dst_rank, slot) + (static_cast<int64_t>(mb) * p.nkb + kb) * kAStageBytes;
-  if (it == 0) {
-    const int b = mb / p.nmb_per_batch;
-    const int row0 = (mb - b * p.nmb_per_batch) * BM;
-    const int valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - row0));
-    const char* xb = p.x + h * p.x_rank_stride +
-                     ((static_cast<int64_t>(b) * p.x_rows + pass * p.Sc + row0) * p.K) * 2;
-#pragma unroll 1
-    for (int u0 = 0; u0 < 32; u0 += 8) {
-      uint4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = (u0 + u) * 32 + lane;  // 16 B chunk id in the 128 x 128 B tile
-        const int row = q >> 3, c16 = q & 7;
-        const int64_t col = static_cast<int64_t>(kb) * BK + c16 * 8;
-        v[u] = (row < valid && col < p.K)
-                   ? *reinterpret_cast<const uint4*>(xb + (row * p.K + col) * 2)
-                   : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int q = (u0 + u) * 32 + lane;
-        const int row = q >> 3, c16 = q & 7;
-        *reinterpret_cast<uint4*>(dst + row * 128 + ((c16 ^ (row & 7)) << 4)) = v[u];
-      }
-    }
-  } else {
-    const uint32_t* f = flag_ptr(p, rank, slot - 1, static_cast<int64_t>(mb) * p.nkb + kb);
-    wait_flag(p, f, rank, slot, mb * p.nkb + kb);
-    __syncwarp();
-    if (p.trace) t_src = globaltimer();
-    const char* src =
-        slot_ptr(p, rank, slot - 1) + (static_cast<int64_t>(mb) * p.nkb + kb) * kAStageBytes;
-#pragma unroll 1
-    for (int u0 = 0; u0 < 32; u0 += 8) {
-      uint4 v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = *reinterpret_cast<const uint4*>(src + ((u0 + u) * 32 + lane) * 16);
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        *reinterpret_cast<uint4*>(dst + ((u0 + u) * 32 + lane) * 16) = v[u];
-    }
-  }
-  fence_sys();
-  __syncwarp();
-  if (lane == 0 && rank != p.fault_rank)
-    st_release_sys(flag_ptr(p, dst_rank, slot, static_cast<int64_t>(mb) * p.nkb + kb), p.epoch);
-  if (lane == 0 && p.trace) trace_rec(p, TR_AG_PIECE, rank, slot, static_cast<int64_t>(mb) * p.nkb + kb, t_src, globaltimer());
-}
-
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_constant__ KParams p) {
@@ -337,7 +277,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   uint64_t* empty = bars + kStages;       // per CTA: 1 (leader's multicast commit)
   uint64_t* tfull = bars + 2 * kStages;   // per CTA: 1 (leader's multicast commit)
   uint64_t* tempty = bars + 2 * kStages + 2;  // leader: 8 epilogue warps of the pair
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * kStages + 4);
+  // per CTA, per forwarder group: a forwarded A stage landed (MMA -> forwarder)
+  uint64_t* fwd_ready = bars + 2 * kStages + 4;  // [2][kStages]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kStages + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -351,6 +293,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   const int per_step = p.npairs * p.nnt;
   const int ntiles = p.nsteps * per_step;
   const bool active = h < p.n_hosted;  // (grid is sized exactly; kept for safety)
+  // AG ring forwarding rides the A pipeline: the stage image is bulk-stored to the
+  // successor before the stage is recycled (so `empty` also waits for the forwarder).
+  const bool fwd = p.op == OP_AG && p.T > 1 && !p.compute_only;
+  const int nfwd = min(p.ag_nfwd, p.nnt);       // leading n-tiles that forward an m-block
+  const int fbatch = min(max(p.ag_batch, 1), 16);  // forwards per fence + flag publication
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tmap_a);
@@ -360,7 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 2);
-      mbar_init(empty + s, 1);
+      mbar_init(empty + s, fwd ? 2 : 1);
+      mbar_init(fwd_ready + s, 1);
+      mbar_init(fwd_ready + kStages + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
@@ -377,45 +326,59 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (!active) {
   } else if (warp == 0) {
     // ===================================================== TMA producer (both CTAs)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int lin = gp; lin < ntiles; lin += GP) {
-        const Tile t = get_tile(p, lin, cta);
-        const int pass = t.step / p.T, it = t.step - pass * p.T;
-        const bool a_from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
-        int64_t arow;
-        if (t.valid == 0)
-          arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
-        else if (p.op == OP_RS)
-          arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
-        else
-          arow = pass * p.Sc + t.row0;
-        const int aslot = pass * (p.T - 1) + it - 1;
-        int ready = -1;  // wire images [0, ready] of this m-block are known to have landed
-        uint64_t t_first = 0;
-        for (int kb = 0; kb < p.nkb; ++kb) {
+    // The whole warp walks the schedule (the wire-image flag scan is warp-parallel);
+    // lane 0 issues barrier arrivals and TMA loads.
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int lin = gp; lin < ntiles; lin += GP) {
+      const Tile t = get_tile(p, lin, cta);
+      const int pass = t.step / p.T, it = t.step - pass * p.T;
+      const bool a_from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
+      int64_t arow;
+      if (t.valid == 0)
+        arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
+      else if (p.op == OP_RS)
+        arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
+      else
+        arow = pass * p.Sc + t.row0;
+      const int aslot = pass * (p.T - 1) + it - 1;
+      const uint32_t* mflags =
+          a_from_wire ? flag_ptr(p, rank, aslot, static_cast<int64_t>(t.mb) * p.nkb) : nullptr;
+      int ready = -1;  // wire images [0, ready] of this m-block are known to have landed
+      uint64_t t_first = 0;
+      const bool fwd_tile = fwd && it < p.T - 1 && t.nt < nfwd;
+      for (int kb = 0; kb < p.nkb; ++kb) {
+        if (a_from_wire && t.valid && kb > ready) {
+          // Wait for image kb, then claim the run of consecutive landed images: every lane
+          // acquire-loads one flag (system scope), the warp barrier carries that ordering to
+          // lane 0, whose proxy fence orders it before the TMA (async-proxy) reads.
+          const uint64_t tw0 = p.trace ? globaltimer() : 0;
+          if (lane == 0) wait_flag(p, mflags + kb, rank, t.step, lin);
+          __syncwarp();
+          ready = kb;
+          while (ready + 1 < p.nkb) {
+            const int k = ready + 1 + lane;
+            const bool ok = k >= p.nkb || ld_acquire_sys(mflags + k) >= p.epoch;
+            const uint32_t m = __ballot_sync(0xffffffffu, ok);
+            const int run = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+            ready = min(ready + run, p.nkb - 1);
+            if (run < 32) break;
+          }
+          __syncwarp();
+          if (lane == 0) fence_proxy_async_global();
+          if (p.trace && lane == 0) {
+            const uint64_t tw1 = globaltimer();
+            if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
+          }
+        }
+        if (lane == 0) {
           mbar_wait(p, empty + stage, phase ^ 1);
+          // Stages the forwarder will not touch: arrive on its behalf (empty counts 2).
+          if (fwd && !(fwd_tile && kb % nfwd == t.nt)) mbar_arrive(empty + stage);
           uint8_t* sa = smem_a + stage * kAStageBytes;
           uint8_t* sb = smem_b + stage * kBStageBytes;
           const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
           const int img = t.mb * p.nkb + kb;
-          if (a_from_wire && t.valid && kb > ready) {
-            // Wait for this image, then claim every consecutive image that has already
-            // landed (relaxed reads of adjacent flag words); one system-scope fence +
-            // proxy fence then orders all of them before the TMA reads.
-            const uint32_t* f = flag_ptr(p, rank, aslot, static_cast<int64_t>(t.mb) * p.nkb);
-            const uint64_t tw0 = p.trace ? globaltimer() : 0;
-            wait_flag(p, f + kb, rank, t.step, lin);
-            if (p.trace) {
-              const uint64_t tw1 = globaltimer();
-              if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
-            }
-            ready = kb;
-            while (ready + 1 < p.nkb && ld_relaxed_sys(f + ready + 1) >= p.epoch) ++ready;
-            fence_sys();
-            fence_proxy_async_global();
-          }
           if (leader)
             mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
           else
@@ -429,10 +392,10 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                             kb * BK, h);
           if (p.trace && kb == 0) t_first = globaltimer();
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        if (p.trace) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
+        if (++stage == kStages) { stage = 0; phase ^= 1; }
       }
+      if (p.trace && lane == 0) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
     }
   } else if (warp == 1) {
     // ===================================================== MMA issuer (leader CTA)
@@ -441,15 +404,28 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
+      int fo = 0;  // ordinal of forwarded stage uses (same sequence in all roles)
       for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
         const int a = lt & 1;
         const uint32_t use = static_cast<uint32_t>(lt >> 1);
         mbar_wait(p, tempty + a, (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + a * BN;
+        int fwd_nt = -1;
+        if (fwd) {
+          const Tile t = get_tile(p, lin, 0);
+          const int it = t.step % p.T;
+          if (it < p.T - 1 && t.nt < nfwd) fwd_nt = t.nt;
+        }
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(p, full + stage, phase);
           tc_fence_after();
+          if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
+            uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kStages + stage;
+            mbar_arrive(fr);
+            mbar_arrive_cluster(mapa_shared(smem_u32(fr), 1));
+            ++fo;
+          }
           const uint32_t abase = smem_u32(smem_a + stage * kAStageBytes);
           const uint32_t bbase = smem_u32(smem_b + stage * kBStageBytes);
 #pragma unroll
@@ -468,17 +444,66 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       }
     }
   } else if (warp == 2 || warp == 3) {
-    // ===================================================== AG ring forwarding
-    if (p.op == OP_AG && p.T > 1 && !p.compute_only) {
-      const int cw = warp - 2;
-      const int per_slot = p.nmb * p.nkb;
-      const int npieces = p.m * (p.T - 1) * per_slot;
-      for (int q = g * 2 + cw; q < npieces; q += G * 2) {
-        const int slot = q / per_slot;
-        const int rem = q - slot * per_slot;
-        const int mb = rem / p.nkb;
-        const int kb = rem - mb * p.nkb;
-        ag_forward_piece(p, h, rank, slot, mb, kb, lane);
+    // ===================================================== AG ring forwarders (warps 2-3)
+    // Forwarded stage uses (tile nt < nfwd, k-block kb % nfwd == nt) are split into batches
+    // of fbatch alternating between the two warps. For each of its uses a warp waits on its
+    // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B A image out of SMEM
+    // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4 into
+    // the successor's slot (NVLink peer stores). At the end of its batch (and of every tile)
+    // the warp fences its stores at system scope and publishes the image flags; while one
+    // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
+    // which keeps the ring's progress argument (step-i images depend only on step i-1).
+    if (fwd) {
+      const int grp = warp - 2;
+      uint32_t* unpub[16];
+      int nunpub = 0;
+      uint32_t ph = 0;  // per-stage phase bits of this group's fwd_ready barriers
+      int fo = 0;
+      auto flush = [&]() {
+        const uint64_t tf0 = p.trace ? globaltimer() : 0;
+        fence_sys();
+        __syncwarp();
+        if (lane == 0 && rank != p.fault_rank)
+          for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], p.epoch);
+        if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
+        nunpub = 0;
+      };
+      int lt = 0;
+      for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+        const Tile t = get_tile(p, lin, cta);
+        const int pass = t.step / p.T, it = t.step - pass * p.T;
+        if (!(it < p.T - 1 && t.nt < nfwd)) continue;
+        const int slot = pass * (p.T - 1) + it;
+        const int dst_rank = p.sched[rank][it][0];
+        const uint64_t t0 = p.trace ? globaltimer() : 0;
+        for (int kb = t.nt; kb < p.nkb; kb += nfwd) {
+          const bool mine = ((fo / fbatch) & 1) == grp;
+          const bool batch_end = (fo % fbatch) == fbatch - 1;
+          ++fo;
+          if (!mine) continue;
+          const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kStages);
+          mbar_wait(p, fwd_ready + grp * kStages + stage, (ph >> stage) & 1u);
+          ph ^= 1u << stage;
+          if (t.valid > 0) {
+            const int64_t img = static_cast<int64_t>(t.mb) * p.nkb + kb;
+            const uint4* src = reinterpret_cast<const uint4*>(smem_a + stage * kAStageBytes);
+            uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, dst_rank, slot) + img * kAStageBytes);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              uint4 v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] = src[(half * 16 + i) * 32 + lane];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) dst[(half * 16 + i) * 32 + lane] = v[i];
+            }
+            unpub[nunpub++] = flag_ptr(p, dst_rank, slot, img);
+          }
+          __syncwarp();  // every lane's SMEM reads of the stage are done
+          if (lane == 0) mbar_arrive(empty + stage);
+          if (batch_end && nunpub > 0) flush();
+        }
+        if (nunpub > 0) flush();
+        if (p.trace && lane == 0 && t.valid > 0) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
       }
     }
   } else {
@@ -490,6 +515,20 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(tempty + 1), 0);
+    // RS flags are published lazily: one system fence covers the wire stores of up to
+    // kPend tiles, and pending flags are always published before any wait that may depend
+    // on a peer (so the ring can never wait on itself).
+    constexpr int kPend = 2;
+    uint32_t* pend[kPend];
+    int npend = 0;
+    auto publish = [&]() {
+      if (npend == 0) return;
+      fence_sys();
+      __syncwarp();
+      if (lane == 0 && rank != p.fault_rank)
+        for (int i = 0; i < npend; ++i) st_relaxed_sys(pend[i], p.epoch);
+      npend = 0;
+    };
     int lt = 0;
     for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
       const Tile t = get_tile(p, lin, cta);
@@ -556,7 +595,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       if (tile_live && !p.direct && it > 0 && !p.compute_only) {
         const int slot_in = slot_send - 1;
         const uint64_t tw0 = (p.trace && lane == 0) ? globaltimer() : 0;
-        wait_flag(p, flag_ptr(p, rank, slot_in, fidx), rank, t.step, lin);
+        const uint32_t* fin = flag_ptr(p, rank, slot_in, fidx);
+        if (npend > 0 && ld_relaxed_sys(fin) < p.epoch) publish();
+        wait_flag(p, fin, rank, t.step, lin);
         if (p.trace && lane == 0 && ew == 0) {
           const uint64_t tw1 = globaltimer();
           if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_IN, rank, t.step, lin, tw0, tw1);
@@ -564,6 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
       }
       if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
+        publish();
         for (int s = 0; s < p.T - 1; ++s)
           wait_flag(p, flag_ptr(p, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin);
       }
@@ -601,15 +643,14 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
       if (!last && tile_live) {
-        fence_sys();
-        __syncwarp();
-        if (lane == 0 && rank != p.fault_rank)
-          st_release_sys(flag_ptr(p, send_rank, slot_send, fidx), p.epoch);
+        pend[npend++] = flag_ptr(p, send_rank, slot_send, fidx);
+        if (npend == kPend) publish();
         if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_FLAG, rank, t.step, lin, t_epi0, globaltimer());
       }
       if (p.trace && lane == 0 && ew == 0 && tile_live)
         trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());
     }
+    publish();
   }
 
   tc_fence_before();

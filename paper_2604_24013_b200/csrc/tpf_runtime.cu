@@ -37,6 +37,12 @@ constexpr int64_t kDefaultTimeoutNs = 10ll * 1000 * 1000 * 1000;
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  const int x = (e && *e) ? std::atoi(e) : dflt;
+  return x > 0 ? x : dflt;
+}
+
 // Raster: m-block pairs that sweep the n-tiles together (L2 reuse of B). 16 pairs =
 // 32 m-blocks = 4096 rows: the 126 MB L2 holds that A panel plus the live B strips.
 int env_group_m() {
@@ -211,6 +217,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.nkb = g.nkb;
   p.npairs = g.npairs;
   p.group_m = env_group_m();
+  p.ag_nfwd = env_int("TPF_AG_NFWD", 4);
+  p.ag_batch = env_int("TPF_AG_BATCH", 4);
   p.nsteps = k.T * k.m;
   p.B = static_cast<int>(k.B);
   p.Sc = k.Sc;

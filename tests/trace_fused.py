@@ -58,3 +58,45 @@ if pieces:
         print(f"  rank0 AG slot {sl}: first src {(a - t_base) / 1e3:8.1f} us  last publish {(b - t_base) / 1e3:8.1f} us  "
               f"mean piece {d / n / 1e3:6.2f} us  n={n}")
 print("no_tail:", trace.no_tail(summ))
+
+# main-loop durations by (forwarding tile?) -- reproduce the kernel's pair-tile raster
+if op == "ag":
+    per_step_pairs = ((S // T + 127) // 128 + 1) // 2
+    nnt = (2 * F // T + 255) // 256
+    GM = int(os.environ.get("TPF_GROUP_M", "16"))
+    nfwd = min(int(os.environ.get("TPF_AG_NFWD", "4")), nnt)
+
+    def nt_of(lin):
+        rem = lin % (per_step_pairs * nnt)
+        g0 = (rem // (GM * nnt)) * GM
+        gm = min(GM, per_step_pairs - g0)
+        return (rem - g0 * nnt) // gm
+
+    ml = [rr for rr in recs if rr.kind == trace.TR_MAINLOOP and rr.rank == 0]
+    fw = [(rr.t1 - rr.t0) / 1e3 for rr in ml if nt_of(rr.index) < nfwd and rr.step < T - 1]
+    nf = [(rr.t1 - rr.t0) / 1e3 for rr in ml if not (nt_of(rr.index) < nfwd and rr.step < T - 1)]
+    print(f"rank0 mainloop(us): forwarding tiles n={len(fw)} mean={sum(fw) / max(1, len(fw)):.1f}  "
+          f"others n={len(nf)} mean={sum(nf) / max(1, len(nf)):.1f}")
+    ep = [(rr.t1 - rr.t0) / 1e3 for rr in recs if rr.kind == trace.TR_TILE and rr.rank == 0]
+    print(f"rank0 epilogue(us): mean={sum(ep) / max(1, len(ep)):.1f} max={max(ep):.1f}")
+    fl = [rr for rr in recs if rr.kind == 7 and rr.rank == 0]
+    if fl:
+        d = sorted((rr.t1 - rr.t0) / 1e3 for rr in fl)
+        print(f"rank0 flush(us): n={len(d)} mean={sum(d) / len(d):.2f} p50={d[len(d) // 2]:.2f} max={d[-1]:.2f} "
+              f"flags/flush={sum(rr.index for rr in fl) / len(fl):.1f}")
+    # producer waits on wire images, by step
+    wa = [rr for rr in recs if rr.kind == trace.TR_WAIT_A and rr.rank == 0]
+    by = {}
+    for rr in wa:
+        by.setdefault(rr.step, [0, 0.0])
+        by[rr.step][0] += 1
+        by[rr.step][1] += (rr.t1 - rr.t0) / 1e3
+    print("rank0 producer wire waits by step (count, total us):", {k: (v[0], round(v[1], 1)) for k, v in sorted(by.items())})
+    # per-pair busy fraction: sum of mainloop spans / kernel span
+    t_base = min(rr.t0 for rr in recs if rr.t0 > 0)
+    t_end = max(rr.t1 for rr in recs)
+    busy = {}
+    for rr in ml:
+        busy[rr.block] = busy.get(rr.block, 0) + (rr.t1 - rr.t0)
+    print(f"rank0 kernel span {(t_end - t_base) / 1e3:.0f} us; mainloop busy per CTA (us): "
+          f"min {min(busy.values()) / 1e3:.0f} max {max(busy.values()) / 1e3:.0f}")
