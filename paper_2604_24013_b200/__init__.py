@@ -178,11 +178,10 @@ class Communicator:
     def from_process_group(cls, sym_bytes: int, group=None) -> "Communicator":
         import torch.distributed as dist
         rank, world = dist.get_rank(group), dist.get_world_size(group)
+        from .dist import exchange_ipc_handles
         comm = cls.create(rank, world, sym_bytes)
         if world > 1:
-            handles = [None] * world
-            dist.all_gather_object(handles, comm.ipc_handle(), group=group)
-            comm.open_peers(handles)
+            comm.open_peers(exchange_ipc_handles(comm.ipc_handle(), group))
             dist.barrier(group)
         return comm
 
