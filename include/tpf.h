@@ -149,6 +149,17 @@ int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
                 int64_t K_local, int64_t N, int kind, int m, int wire_dtype, int out_dtype,
                 void* stream);
 
+/* DP gradient sync (BASELINE cfg 4): reduce-scatter of the weight
+ * gradient fused into its GEMM. Computes dW = sum_ranks X_r^T . dY_r (K x N) and
+ * leaves rows [r*K/T, (r+1)*K/T) on rank r -- exactly
+ *   fuse_reduce_scatter(x = X_r^T as (1, K, M_local), f = matmul(., dY_r), schedule, m)
+ * (collectives.cpp:362-405), reduction order per schedule. X^T is read MN-major
+ * straight from row-major X (no transpose).
+ *   X  : bf16 (M_local, K) row-major     dY : bf16 (M_local, N) row-major
+ *   dW : (K/T, N) row-major, out_dtype */
+int tpf_dp_grad_rs(tpf_comm* c, const void* X, const void* dY, void* dW, int64_t M_local, int64_t K,
+                   int64_t N, int kind, int m, int wire_dtype, int out_dtype, void* stream);
+
 /* T == 1 degenerate case of both ops (collectives.cpp:242,379): out = a * b.
  *   a: bf16 (M, K), b: bf16 (K, N), out: (M, N) out_dtype. No communicator. */
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

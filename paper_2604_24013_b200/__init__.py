@@ -72,6 +72,7 @@ _lib.tpf_comm_set_trace.argtypes = [_vp, _vp, _i64]
 _lib.tpf_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 3 + [_vp]
 _lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + [_vp]
 _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
+_lib.tpf_dp_grad_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int] * 4 + [_vp]
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
 _lib.tpf_sym_bytes_ag.argtypes = [C.c_int] + [_i64] * 4 + [C.c_int]
 _lib.tpf_sym_bytes_ag.restype = _i64
@@ -82,7 +83,7 @@ EXPORTED_SYMBOLS = (
     "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
     "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
     "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_gemm",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_gemm",
     "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
 )
 
@@ -251,6 +252,19 @@ def interleave_gate_up(gate, up, tile: int = 256):
     assert up.shape == gate.shape and F % half == 0
     return torch.stack([gate.reshape(K, F // half, half), up.reshape(K, F // half, half)],
                        dim=2).reshape(K, 2 * F)
+
+
+def _dp_grad_rs(self, X, dY, dW, kind: int = RING, m: int = 1, wire: int = F32, stream=None) -> None:
+    """DP gradient reduce-scatter fused into the weight-gradient GEMM (cfg 4):
+    dW_r = rows [r*K/T, (r+1)*K/T) of sum_q X_q^T dY_q. Per rank X: (M_local, K), dY: (M_local, N),
+    dW: (K/T, N); a local group takes rank-stacked tensors."""
+    M_local, K = X.shape[-2:]
+    N = dY.shape[-1]
+    _check(_lib.tpf_dp_grad_rs(self._h, X.data_ptr(), dY.data_ptr(), dW.data_ptr(), M_local, K, N, kind, m,
+                               wire, _dtype_code(dW), _stream_ptr(stream)))
+
+
+Communicator.dp_grad_rs = _dp_grad_rs
 
 
 def _dtype_code(t) -> int:

@@ -27,7 +27,7 @@ enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };
 constexpr int kErrWords = 8;
 
 struct KParams {
-  CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks)
+  CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); a_mn: (rows, K, B, ranks)
   CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B)
   CUtensorMap tmap_wire;  // AG wire images (128 B, 128 rows, image, slot, hosted rank), no swizzle
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
@@ -41,6 +41,7 @@ struct KParams {
   int ag_nfwd;         // AG: leading n-tiles of an m-block that forward its images
   int ag_batch;        // AG: forwards per fence + flag publication (<= 16)
   int act;             // AG epilogue activation (Act)
+  int a_mn;            // A operand MN-major (rows contiguous): x stored as (K_red, rows), e.g. X for X^T dY
   int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
   int out_f32;         // output dtype: 1 fp32, 0 bf16
   int nmb_per_batch;   // ceil(Sc / BM)

@@ -383,10 +383,17 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
           else
             mbar_arrive_cluster(fb);
-          if (a_from_wire)
+          if (a_from_wire) {
             tma_load_2sm_5d(sa, &p.tmap_wire, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
-          else
+          } else if (p.a_mn) {
+            // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
+#pragma unroll
+            for (int q = 0; q < BM / 64; ++q)
+              tma_load_2sm_4d(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
+                              t.b, h);
+          } else {
             tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
+          }
 #pragma unroll
           for (int q = 0; q < BN / 128; ++q)
             tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
@@ -400,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   } else if (warp == 1) {
     // ===================================================== MMA issuer (leader CTA)
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/true);
+      const uint32_t idesc = make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/true, /*a_mn_major=*/p.a_mn != 0);
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
@@ -431,7 +438,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
-            const uint64_t ad = make_sdesc(abase + k * 32, 0, 1024);
+            // MN-major A: like B, 16 K-rows = 2048 B, LBO = 64-row atom (8 KiB), SBO = 1 KiB.
+            const uint64_t ad = p.a_mn ? make_sdesc(abase + k * 2048, 64 * BK * 2, 1024)
+                                       : make_sdesc(abase + k * 32, 0, 1024);
             // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
             // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
             const uint64_t bd = make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);

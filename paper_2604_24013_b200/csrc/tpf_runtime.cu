@@ -168,6 +168,7 @@ struct Call {
   int op, T, m, direct, act, wire_f32, out_f32, n_hosted, rank0;
   int64_t B, Sc, K, N, x_rows, out_rows;
   int64_t N_gemm;  // columns of W (B operand); == N unless the epilogue narrows (SwiGLU)
+  int a_mn;        // x is stored (K, rows): A = x^T read MN-major (DP: X^T dY without a transpose)
   const void* x;
   const void* w;
   void* out;
@@ -183,7 +184,16 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   const int64_t x_rank_stride = k.B * k.x_rows * k.K * 2;
   const int64_t w_rank_stride = k.K * NG * 2;
   const int64_t esz = k.out_f32 ? 4 : 2;
-  {
+  if (k.a_mn) {
+    const uint64_t dims[4] = {static_cast<uint64_t>(k.x_rows), static_cast<uint64_t>(k.K),
+                              static_cast<uint64_t>(k.B), static_cast<uint64_t>(R)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(k.x_rows * 2),
+                                 static_cast<uint64_t>(k.x_rows * k.K * 2),
+                                 static_cast<uint64_t>(x_rank_stride)};
+    const uint32_t box[4] = {64, tpf::BK, 1, 1};
+    tpf::Status s = make_tmap(&p.tmap_a, k.x, 4, dims, strides, box);
+    if (!s.good()) return s;
+  } else {
     const uint64_t dims[4] = {static_cast<uint64_t>(k.K), static_cast<uint64_t>(k.x_rows),
                               static_cast<uint64_t>(k.B), static_cast<uint64_t>(R)};
     const uint64_t strides[3] = {static_cast<uint64_t>(k.K * 2),
@@ -209,6 +219,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.n_hosted = R;
   p.rank0 = k.rank0;
   p.act = k.act;
+  p.a_mn = k.a_mn;
   p.wire_f32 = k.wire_f32;
   p.out_f32 = k.out_f32;
   p.nmb_per_batch = g.nmb_per_batch;
@@ -505,6 +516,44 @@ int64_t tpf_sym_bytes_rs(int world, int64_t B, int64_t S, int64_t K_local, int64
   const int64_t slot =
       static_cast<int64_t>(g.nmb) * g.nnt * tpf::BM * tpf::BN * (wire_dtype == TPF_F32 ? 4 : 2);
   return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(m) * (world - 1) * slot;
+}
+
+int tpf_dp_grad_rs(tpf_comm* c, const void* X, const void* dY, void* dW, int64_t M_local, int64_t K,
+                   int64_t N, int kind, int m, int wire_dtype, int out_dtype, void* stream) {
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  if (m < 1) return fail(tpf::Status::invalid("fuse_reduce_scatter: granularity must be >= 1"));
+  if (m > 1 && kind != TPF_RING)
+    return fail(tpf::Status::invalid(
+        "fuse_reduce_scatter: granularity > 1 is supported for the ring schedule only"));
+  std::vector<int32_t> sched;
+  s = tpf::build_schedule(kind, T, sched);
+  if (!s.good()) return fail(s);
+  if (M_local < 1 || K < 1 || N < 1)
+    return fail(tpf::Status::shape("dp_grad_rs: dimensions must be positive"));
+  if (T > 1 && K % (static_cast<int64_t>(T) * m))
+    return fail(tpf::Status::invalid("fuse_reduce_scatter: sequence length " + std::to_string(K) +
+                                     " is not divisible by " + std::to_string(T * m) + " (group size " +
+                                     std::to_string(T) + " x granularity " + std::to_string(m) + ")"));
+  if (K % 8 || N % 8) return fail(tpf::Status::shape("dp_grad_rs: K and N must be multiples of 8"));
+  Call k{};
+  k.op = tpf::OP_RS;
+  k.T = T;
+  k.m = T > 1 ? m : 1;
+  k.direct = kind == TPF_PAIRWISE;
+  k.wire_f32 = wire_dtype == TPF_F32;
+  k.out_f32 = out_dtype == TPF_F32;
+  k.n_hosted = hosted(c);
+  k.rank0 = c->local_group ? 0 : c->rank;
+  k.a_mn = 1;
+  // x = X_r^T seen as (1, K, M_local): "sequence" rows = K (dW rows), reduction = M_local
+  k.B = 1; k.Sc = K / (static_cast<int64_t>(T) * k.m); k.K = M_local; k.N = N;
+  k.x_rows = K; k.out_rows = K / T;
+  k.x = X; k.w = dY; k.out = dW;
+  k.sched = T > 1 ? sched.data() : nullptr;
+  s = launch(c, k, static_cast<cudaStream_t>(stream));
+  return s.good() ? TPF_OK : fail(s);
 }
 
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

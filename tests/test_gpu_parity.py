@@ -405,3 +405,57 @@ def test_ag_gemm_fused_swiglu(T):
         ref = torch.nn.functional.silu(gg) * uu
         err = (out[r].reshape(B * S, fl) - ref).abs().max().item()
         assert err <= 1e-3 * ref.abs().max().item() + 1e-5, (r, err)
+
+
+# ------------------------------------------------ DP gradient sync (cfg 4, a19)
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+def test_dp_grad_rs_exact(T):
+    """dW = sum_q X_q^T dY_q reduce-scattered by rows: equals the oracle's
+    fuse_reduce_scatter over the per-rank fp64 partials, bit for bit on integer data."""
+    M, K, N = 96, 64 * T, 136
+    kinds = [tpf.RING, tpf.CIRCULAR] + ([tpf.PAIRWISE] if T % 2 == 0 or T == 1 else [])
+    X = np.stack([O.randint((M, K), 0, 5, 60 + r) for r in range(T)])
+    dY = np.stack([O.randint((M, N), -2, 2, 70 + r) for r in range(T)])
+    parts = np.stack([(X[r].T @ dY[r])[None] for r in range(T)])  # (T, 1, K, N), exact ints
+    Xd = torch.stack([bf16(X[r]) for r in range(T)]).to(DEV)
+    dYd = torch.stack([bf16(dY[r]) for r in range(T)]).to(DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, 1, K, M, N, 2))
+    for kind in kinds:
+        for m in ((1, 2) if kind == tpf.RING and T > 1 else (1,)):
+            dW = torch.full((T, K // T, N), float("nan"), device=DEV)
+            comm.dp_grad_rs(Xd, dYd, dW, kind=kind, m=m)
+            comm.sync()
+            want = O.fuse_rs_identity(T, kind, m, parts)[:, 0]
+            assert np.array_equal(dW.double().cpu().numpy(), want), (kind, m)
+    comm.close()
+
+
+def test_dp_grad_rs_full_size_replay():
+    """cfg 4 shapes (a Llama-3.2-1B-class MLP weight, 8 DP ranks, 4096 tokens/rank):
+    bf16 wire ring RS of dW is bit-exact vs an fp32 replay of the ring order over the
+    library's own single-rank partials."""
+    T, M, K, N = 8, 4096, 2048, 8192
+    g = torch.Generator(device=DEV).manual_seed(3)
+    X = torch.randn((T, M, K), device=DEV, generator=g).to(torch.bfloat16)
+    dY = (torch.randn((T, M, N), device=DEV, generator=g) / 64).to(torch.bfloat16)
+    dW = torch.empty((T, K // T, N), device=DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, 1, K, M, N, 1, tpf.BF16))
+    comm.dp_grad_rs(X, dY, dW, kind=tpf.RING, wire=tpf.BF16)
+    comm.sync()
+    comm.close()
+    one = tpf.Communicator.create(0, 1, 0)
+    full = []
+    for q in range(T):
+        o = torch.empty((K, N), device=DEV)
+        one.dp_grad_rs(X[q], dY[q], o)
+        full.append(o)
+    one.sync()
+    one.close()
+    sched = tpf.build_schedule(tpf.RING, T)
+    kl = K // T
+    for r in (0, 5):
+        chain = [next(q for q in range(T) if sched[q][i][2] == r) for i in range(T)]
+        acc = full[chain[0]][r * kl:(r + 1) * kl]
+        for q in chain[1:]:
+            acc = full[q][r * kl:(r + 1) * kl] + acc.to(torch.bfloat16).float()
+        assert torch.equal(dW[r], acc), r
