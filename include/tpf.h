@@ -160,6 +160,17 @@ int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
 int tpf_dp_grad_rs(tpf_comm* c, const void* X, const void* dY, void* dW, int64_t M_local, int64_t K,
                    int64_t N, int kind, int m, int wire_dtype, int out_dtype, void* stream);
 
+/* DP parameter all-gather fused into the forward GEMM (BASELINE cfg 4, a19): the
+ * ring (ring_indices_ag) carries weight row blocks instead of activation chunks.
+ * Rank r holds rows [r*N_local, (r+1)*N_local) of W (N x K, PyTorch Linear layout);
+ * every rank computes its full output y = x . W^T, block l of the output columns in
+ * ring step i with l = (r - i) mod T (fuse_all_gather order, collectives.cpp:237-279).
+ *   x     : bf16 (M_local, K) row-major     w_rows : bf16 (N_local, K) row-major
+ *   out   : (M_local, T*N_local) row-major, out_dtype */
+int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* out, int64_t M_local,
+                         int64_t K, int64_t N_local, int out_dtype, void* stream);
+int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local);
+
 /* T == 1 degenerate case of both ops (collectives.cpp:242,379): out = a * b.
  *   a: bf16 (M, K), b: bf16 (K, N), out: (M, N) out_dtype. No communicator. */
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

@@ -73,6 +73,9 @@ _lib.tpf_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 3 + 
 _lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + [_vp]
 _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
 _lib.tpf_dp_grad_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int] * 4 + [_vp]
+_lib.tpf_dp_param_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
+_lib.tpf_sym_bytes_dp_ag.argtypes = [C.c_int, _i64, _i64]
+_lib.tpf_sym_bytes_dp_ag.restype = _i64
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
 _lib.tpf_sym_bytes_ag.argtypes = [C.c_int] + [_i64] * 4 + [C.c_int]
 _lib.tpf_sym_bytes_ag.restype = _i64
@@ -83,7 +86,7 @@ EXPORTED_SYMBOLS = (
     "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
     "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
     "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_gemm",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_dp_param_ag_gemm", "tpf_sym_bytes_dp_ag", "tpf_gemm",
     "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
 )
 
@@ -265,6 +268,23 @@ def _dp_grad_rs(self, X, dY, dW, kind: int = RING, m: int = 1, wire: int = F32, 
 
 
 Communicator.dp_grad_rs = _dp_grad_rs
+
+
+def _dp_param_ag_gemm(self, x, w_rows, out, stream=None) -> None:
+    """DP parameter all-gather fused into the forward GEMM (cfg 4, a19): out = x . W^T where
+    W (N x K) is row-sharded over the ranks (PyTorch Linear layout). Per rank x: (M_local, K),
+    w_rows: (N/T, K), out: (M_local, N); a local group takes rank-stacked tensors."""
+    M_local, K = x.shape[-2:]
+    N_local = w_rows.shape[-2]
+    _check(_lib.tpf_dp_param_ag_gemm(self._h, x.data_ptr(), w_rows.data_ptr(), out.data_ptr(), M_local, K,
+                                     N_local, _dtype_code(out), _stream_ptr(stream)))
+
+
+Communicator.dp_param_ag_gemm = _dp_param_ag_gemm
+
+
+def sym_bytes_dp_ag(world, K, N_local) -> int:
+    return int(_lib.tpf_sym_bytes_dp_ag(world, K, N_local))
 
 
 def _dtype_code(t) -> int:

@@ -28,7 +28,7 @@ constexpr int kErrWords = 8;
 
 struct KParams {
   CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); a_mn: (rows, K, B, ranks)
-  CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B)
+  CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); b_kmajor: (K, N, ranks)
   CUtensorMap tmap_wire;  // AG wire images (128 B, 128 rows, image, slot, hosted rank), no swizzle
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
   int T;               // group size
@@ -42,6 +42,10 @@ struct KParams {
   int ag_batch;        // AG: forwards per fence + flag publication (<= 16)
   int act;             // AG epilogue activation (Act)
   int a_mn;            // A operand MN-major (rows contiguous): x stored as (K_red, rows), e.g. X for X^T dY
+  int b_kmajor;        // B operand K-major: w stored (N, K) row-major (PyTorch Linear weight layout)
+  int gather_b;        // OP_AG variant: the ring carries B (weight column blocks), not A (DP param AG)
+  int64_t out_ld;      // output row stride (elements)
+  int64_t blk_cols;    // gather_b: columns of one rank's weight block (output column offset unit)
   int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
   int out_f32;         // output dtype: 1 fp32, 0 bf16
   int nmb_per_batch;   // ceil(Sc / BM)

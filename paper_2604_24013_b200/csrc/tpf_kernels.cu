@@ -333,22 +333,30 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     for (int lin = gp; lin < ntiles; lin += GP) {
       const Tile t = get_tile(p, lin, cta);
       const int pass = t.step / p.T, it = t.step - pass * p.T;
-      const bool a_from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
+      const bool from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
+      const bool a_from_wire = from_wire && !p.gather_b;
+      const bool b_from_wire = from_wire && p.gather_b;
       int64_t arow;
       if (t.valid == 0)
         arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
       else if (p.op == OP_RS)
         arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
+      else if (p.gather_b)
+        arow = t.row0;
       else
         arow = pass * p.Sc + t.row0;
       const int aslot = pass * (p.T - 1) + it - 1;
-      const uint32_t* mflags =
-          a_from_wire ? flag_ptr(p, rank, aslot, static_cast<int64_t>(t.mb) * p.nkb) : nullptr;
-      int ready = -1;  // wire images [0, ready] of this m-block are known to have landed
+      // wire images of this CTA's operand for this tile: A rows (m-block) or B half (n-tile)
+      const int64_t img0 = p.gather_b ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
+                                      : static_cast<int64_t>(t.mb) * p.nkb;
+      const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
+      const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, rank, aslot, img0) : nullptr;
+      int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
       uint64_t t_first = 0;
-      const bool fwd_tile = fwd && it < p.T - 1 && t.nt < nfwd;
+      const int fwd_key = p.gather_b ? (t.mb >> 1) : t.nt;  // which tiles forward (pair / n-tile)
+      const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
       for (int kb = 0; kb < p.nkb; ++kb) {
-        if (a_from_wire && t.valid && kb > ready) {
+        if (wire_live && kb > ready) {
           // Wait for image kb, then claim the run of consecutive landed images: every lane
           // acquire-loads one flag (system scope), the warp barrier carries that ordering to
           // lane 0, whose proxy fence orders it before the TMA (async-proxy) reads.
@@ -374,11 +382,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (lane == 0) {
           mbar_wait(p, empty + stage, phase ^ 1);
           // Stages the forwarder will not touch: arrive on its behalf (empty counts 2).
-          if (fwd && !(fwd_tile && kb % nfwd == t.nt)) mbar_arrive(empty + stage);
+          if (fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
           uint8_t* sa = smem_a + stage * kAStageBytes;
           uint8_t* sb = smem_b + stage * kBStageBytes;
           const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
-          const int img = t.mb * p.nkb + kb;
+          const int img = static_cast<int>(img0) + kb;
           if (leader)
             mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
           else
@@ -394,10 +402,17 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           } else {
             tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
           }
+          if (b_from_wire) {
+            tma_load_2sm_5d(sb, &p.tmap_wire, fb, 0, 0, img, aslot, h);
+          } else if (p.b_kmajor) {
+            // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
+            tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
+          } else {
 #pragma unroll
-          for (int q = 0; q < BN / 128; ++q)
-            tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
-                            kb * BK, h);
+            for (int q = 0; q < BN / 128; ++q)
+              tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                              kb * BK, h);
+          }
           if (p.trace && kb == 0) t_first = globaltimer();
         }
         if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -407,7 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   } else if (warp == 1) {
     // ===================================================== MMA issuer (leader CTA)
     if (leader && lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/true, /*a_mn_major=*/p.a_mn != 0);
+      const uint32_t idesc =
+          make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/p.b_kmajor == 0 && p.gather_b == 0, /*a_mn_major=*/p.a_mn != 0);
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
@@ -422,7 +438,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (fwd) {
           const Tile t = get_tile(p, lin, 0);
           const int it = t.step % p.T;
-          if (it < p.T - 1 && t.nt < nfwd) fwd_nt = t.nt;
+          const int key = p.gather_b ? (t.mb >> 1) : t.nt;
+          if (it < p.T - 1 && key < nfwd) fwd_nt = key;
         }
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(p, full + stage, phase);
@@ -443,7 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                                        : make_sdesc(abase + k * 32, 0, 1024);
             // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
             // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
-            const uint64_t bd = make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
+            const uint64_t bd = (p.b_kmajor || p.gather_b) ? make_sdesc(bbase + k * 32, 0, 1024)
+                                                           : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
             mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
           mma_commit_2sm(empty + stage, 0x3);
@@ -481,11 +499,17 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
-        if (!(it < p.T - 1 && t.nt < nfwd)) continue;
+        const int key = p.gather_b ? (t.mb >> 1) : t.nt;
+        if (!(it < p.T - 1 && key < nfwd)) continue;
         const int slot = pass * (p.T - 1) + it;
         const int dst_rank = p.sched[rank][it][0];
         const uint64_t t0 = p.trace ? globaltimer() : 0;
-        for (int kb = t.nt; kb < p.nkb; kb += nfwd) {
+        // forwarded operand: this CTA's A rows, or (gather_b) its half of the B tile
+        const bool live = p.gather_b ? true : t.valid > 0;
+        const int64_t img0 = p.gather_b ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
+                                        : static_cast<int64_t>(t.mb) * p.nkb;
+        const uint8_t* sbase = p.gather_b ? smem_b : smem_a;
+        for (int kb = key; kb < p.nkb; kb += nfwd) {
           const bool mine = ((fo / fbatch) & 1) == grp;
           const bool batch_end = (fo % fbatch) == fbatch - 1;
           ++fo;
@@ -493,9 +517,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kStages);
           mbar_wait(p, fwd_ready + grp * kStages + stage, (ph >> stage) & 1u);
           ph ^= 1u << stage;
-          if (t.valid > 0) {
-            const int64_t img = static_cast<int64_t>(t.mb) * p.nkb + kb;
-            const uint4* src = reinterpret_cast<const uint4*>(smem_a + stage * kAStageBytes);
+          if (live) {
+            const int64_t img = img0 + kb;
+            const uint4* src = reinterpret_cast<const uint4*>(sbase + stage * kAStageBytes);
             uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, dst_rank, slot) + img * kAStageBytes);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
@@ -512,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           if (batch_end && nunpub > 0) flush();
         }
         if (nunpub > 0) flush();
-        if (p.trace && lane == 0 && t.valid > 0) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
+        if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
       }
     }
   } else {
@@ -555,9 +579,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 
       if (p.op == OP_AG) {
         const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
-        const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows +
-                             (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
-        char* rp = out_h + orow * p.N * esz;
+        // gather_b: rows stay local, the step selects the output column block l
+        const int64_t orow = p.gather_b ? static_cast<int64_t>(t.b) * p.out_rows + t.row0 + row
+                                        : static_cast<int64_t>(t.b) * p.out_rows +
+                                              (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
+        char* rp = out_h + (orow * p.out_ld + (p.gather_b ? static_cast<int64_t>(l) * p.blk_cols : 0)) * esz;
         if (p.act == ACT_SWIGLU) {
           // Tile-interleaved W: columns [0,128) of the tile are gate, [128,256) the matching
           // up columns -> 128 output columns silu(gate) * up (Llama MLP, fused).
@@ -622,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       char* dst_tile =
           (last || !tile_live) ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
       const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows + pass * p.Sc + t.row0 + row;
-      char* rp = out_h + orow * p.N * esz;
+      char* rp = out_h + orow * p.out_ld * esz;
       for (int j = 0; j < BN / 32; ++j) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + j * 32, r);

@@ -169,6 +169,9 @@ struct Call {
   int64_t B, Sc, K, N, x_rows, out_rows;
   int64_t N_gemm;  // columns of W (B operand); == N unless the epilogue narrows (SwiGLU)
   int a_mn;        // x is stored (K, rows): A = x^T read MN-major (DP: X^T dY without a transpose)
+  int b_kmajor;    // w is stored (N, K) (PyTorch Linear layout): K-major B
+  int gather_b;    // AG ring carries weight column blocks (DP param all-gather)
+  int64_t out_ld;  // output row stride (0: N)
   const void* x;
   const void* w;
   void* out;
@@ -203,7 +206,15 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     tpf::Status s = make_tmap(&p.tmap_a, k.x, 4, dims, strides, box);
     if (!s.good()) return s;
   }
-  {
+  const int64_t out_ld = k.out_ld > 0 ? k.out_ld : k.N;
+  if (k.b_kmajor || k.gather_b) {
+    const uint64_t dims[3] = {static_cast<uint64_t>(k.K), static_cast<uint64_t>(NG),
+                              static_cast<uint64_t>(R)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(k.K * 2), static_cast<uint64_t>(w_rank_stride)};
+    const uint32_t box[3] = {tpf::BK, tpf::BN / 2, 1};
+    tpf::Status s = make_tmap(&p.tmap_b, k.w, 3, dims, strides, box);
+    if (!s.good()) return s;
+  } else {
     const uint64_t dims[3] = {static_cast<uint64_t>(NG), static_cast<uint64_t>(k.K),
                               static_cast<uint64_t>(R)};
     const uint64_t strides[2] = {static_cast<uint64_t>(NG * 2),
@@ -220,6 +231,10 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.rank0 = k.rank0;
   p.act = k.act;
   p.a_mn = k.a_mn;
+  p.b_kmajor = k.b_kmajor;
+  p.gather_b = k.gather_b;
+  p.out_ld = out_ld;
+  p.blk_cols = k.N;
   p.wire_f32 = k.wire_f32;
   p.out_f32 = k.out_f32;
   p.nmb_per_batch = g.nmb_per_batch;
@@ -240,7 +255,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.x = static_cast<const char*>(k.x);
   p.x_rank_stride = x_rank_stride;
   p.out = static_cast<char*>(k.out);
-  p.out_rank_stride = k.B * k.out_rows * k.N * esz;
+  p.out_rank_stride = k.B * k.out_rows * out_ld * esz;
   p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
   p.fault_rank = c ? c->fault_rank : -1;
   p.compute_only = c ? c->compute_only : 0;
@@ -257,8 +272,10 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
       slot_bytes = static_cast<int64_t>(g.nmb) * g.nnt * tpf::BM * tpf::BN * (k.wire_f32 ? 4 : 2);
       flags_per_slot = static_cast<int64_t>(g.nmb) * g.nnt * 4;
     } else {
-      slot_bytes = static_cast<int64_t>(g.nmb) * g.nkb * tpf::kAStageBytes;
-      flags_per_slot = static_cast<int64_t>(g.nmb) * g.nkb;
+      // AG wire images: A rows per (m-block, k-block), or (gather_b) B halves per (half, n-tile, k-block)
+      const int64_t nimg = k.gather_b ? 2ll * g.nnt * g.nkb : static_cast<int64_t>(g.nmb) * g.nkb;
+      slot_bytes = nimg * tpf::kAStageBytes;
+      flags_per_slot = nimg;
     }
     const int64_t data_cap = data_bytes_per_parity(c->sym_bytes);
     if (nslots * slot_bytes > data_cap)
@@ -278,7 +295,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     if (k.op == tpf::OP_AG) {
       // AG wire images of the hosted ranks' local slots: (128 B, 128 rows, image, slot, rank)
       const int64_t rank_stride = R > 1 ? static_cast<int64_t>(c->sym_bytes) : nslots * slot_bytes;
-      const uint64_t dims[5] = {64, tpf::BM, static_cast<uint64_t>(g.nmb) * g.nkb,
+      const uint64_t dims[5] = {64, tpf::BM, static_cast<uint64_t>(flags_per_slot),
                                 static_cast<uint64_t>(nslots), static_cast<uint64_t>(R)};
       const uint64_t strides[4] = {128, tpf::kAStageBytes, static_cast<uint64_t>(slot_bytes),
                                    static_cast<uint64_t>(rank_stride)};
@@ -509,6 +526,12 @@ int64_t tpf_sym_bytes_ag(int world, int64_t B, int64_t S, int64_t K, int64_t N_l
   return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(m) * (world - 1) * slot;
 }
 
+int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local) {
+  if (world <= 1) return 0;
+  const int64_t slot = 2 * ceil_div(N_local, tpf::BN) * ceil_div(K, tpf::BK) * tpf::kAStageBytes;
+  return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(world - 1) * slot;
+}
+
 int64_t tpf_sym_bytes_rs(int world, int64_t B, int64_t S, int64_t K_local, int64_t N, int m,
                          int wire_dtype) {
   if (world <= 1) return 0;
@@ -552,6 +575,37 @@ int tpf_dp_grad_rs(tpf_comm* c, const void* X, const void* dY, void* dW, int64_t
   k.x_rows = K; k.out_rows = K / T;
   k.x = X; k.w = dY; k.out = dW;
   k.sched = T > 1 ? sched.data() : nullptr;
+  s = launch(c, k, static_cast<cudaStream_t>(stream));
+  return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* out, int64_t M_local,
+                         int64_t K, int64_t N_local, int out_dtype, void* stream) {
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  if (M_local < 1 || K < 1 || N_local < 1)
+    return fail(tpf::Status::shape("dp_param_ag_gemm: dimensions must be positive"));
+  if (K % 8 || N_local % 8) return fail(tpf::Status::shape("dp_param_ag_gemm: K and N_local must be multiples of 8"));
+  std::vector<int32_t> sched;
+  Call k{};
+  k.op = tpf::OP_AG;
+  k.T = T;
+  k.m = 1;
+  k.out_f32 = out_dtype == TPF_F32;
+  k.n_hosted = hosted(c);
+  k.rank0 = c->local_group ? 0 : c->rank;
+  k.gather_b = 1;
+  k.b_kmajor = 1;
+  k.B = 1; k.Sc = M_local; k.K = K; k.N = N_local; k.x_rows = M_local; k.out_rows = M_local;
+  k.out_ld = N_local * T;
+  k.x = x; k.w = w_rows; k.out = out;
+  if (T > 1) {
+    sched.resize(static_cast<size_t>(T) * T * 3);
+    for (int r = 0; r < T; ++r)
+      for (int i = 0; i < T; ++i) tpf::ring_indices(false, r, i, T, &sched[(r * T + i) * 3]);
+    k.sched = sched.data();
+  }
   s = launch(c, k, static_cast<cudaStream_t>(stream));
   return s.good() ? TPF_OK : fail(s);
 }

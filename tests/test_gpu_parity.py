@@ -459,3 +459,49 @@ def test_dp_grad_rs_full_size_replay():
         for q in chain[1:]:
             acc = full[q][r * kl:(r + 1) * kl] + acc.to(torch.bfloat16).float()
         assert torch.equal(dW[r], acc), r
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+@pytest.mark.parametrize("shape", [(96, 200, 136), (512, 256, 512)])
+def test_dp_param_ag_gemm_exact(T, shape):
+    """DP parameter all-gather fused into the forward GEMM (cfg 4, a19): every rank's
+    out = x_r . W^T with W row-sharded (PyTorch Linear layout), ring order
+    (ring_indices_ag); exact on integer data; ragged M/K/N edges included."""
+    M, K, Nl = shape
+    N = Nl * T
+    x = np.stack([O.randint((M, K), 0, 5, 80 + r) for r in range(T)])
+    W = O.randint((N, K), -2, 2, 90)
+    xd = torch.stack([bf16(x[r]) for r in range(T)]).to(DEV)
+    wd = torch.stack([bf16(W[r * Nl:(r + 1) * Nl]) for r in range(T)]).to(DEV)
+    out = torch.full((T, M, N), float("nan"), device=DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_dp_ag(T, K, Nl))
+    for _ in range(2):  # twice: epoch / parity reuse
+        comm.dp_param_ag_gemm(xd, wd, out)
+        comm.sync()
+        got = out.double().cpu().numpy()
+        for r in range(T):
+            assert np.array_equal(got[r], x[r] @ W.T), r
+    comm.close()
+
+
+def test_dp_param_ag_gemm_full_size():
+    """cfg 4 shapes (8 DP ranks, 4096 tokens/rank, a 2048 x 8192 weight row-sharded):
+    bit-exact vs a single-rank call on the gathered weight."""
+    T, M, K, N = 8, 4096, 2048, 8192
+    g = torch.Generator(device=DEV).manual_seed(5)
+    x = torch.randn((T, M, K), device=DEV, generator=g).to(torch.bfloat16)
+    W = (torch.randn((N, K), device=DEV, generator=g) / 45).to(torch.bfloat16)
+    out = torch.empty((T, M, N), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_dp_ag(T, K, N // T))
+    comm.dp_param_ag_gemm(x, W.reshape(T, N // T, K).contiguous(), out)
+    comm.sync()
+    comm.close()
+    one = tpf.Communicator.create(0, 1, 0)
+    for r in (0, 6):
+        ref = torch.empty((M, N), device=DEV, dtype=torch.bfloat16)
+        one.dp_param_ag_gemm(x[r], W, ref)
+        one.sync()
+        assert torch.equal(out[r], ref), r
+    ref32 = x[0].float() @ W.float().T
+    assert (out[0].float() - ref32).abs().max().item() <= 2e-2 * ref32.abs().max().item()
+    one.close()
