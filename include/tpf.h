@@ -171,6 +171,19 @@ int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* o
                          int64_t K, int64_t N_local, int out_dtype, void* stream);
 int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local);
 
+/* UP / Ulysses attention with the output all-to-all fused (BASELINE cfg 5).
+ * Replaces: Tensor fuse_all_to_all_attention(RankEndpoint&, const AttentionInputs&,
+ *           const AttentionOptions&) (layers.hpp:100-101, layers.cpp:174-218).
+ * Per rank (head group of `heads` heads, full sequence, Ulysses layout):
+ *   q, k, v : bf16 (batch*heads, S, Dh)
+ *   out     : bf16 (batch, S/T, T*heads*Dh) = concat_feat over source rank of merge_heads
+ * Iteration i computes query slice l = (r+i+1) % T (softmax(q k^T * scale) v, scale =
+ * 1/sqrt(Dh) if `scale`) on the tcgen05 GEMM family; the P.V epilogue pushes every output
+ * tile straight into rank l's buffer at this rank's feature block and flags it; the own
+ * slice is computed last (no trailing transfer). Non-causal, no GQA. */
+int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
+                      int64_t heads, int64_t S, int64_t Dh, int scale, void* stream);
+
 /* T == 1 degenerate case of both ops (collectives.cpp:242,379): out = a * b.
  *   a: bf16 (M, K), b: bf16 (K, N), out: (M, N) out_dtype. No communicator. */
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

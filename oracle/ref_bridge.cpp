@@ -238,3 +238,25 @@ int ref_time_ops(int t, int64_t b, int64_t s, int64_t k_ag, int64_t n_ag, int64_
 }
 
 }  // extern "C"
+
+extern "C" int ref_attention_a2a(int t, int batch, int heads, int64_t s, int64_t dh, int scale,
+                                 const double* q, const double* k, const double* v, double* out) {
+  return guarded([&] {
+    const int64_t bh = static_cast<int64_t>(batch) * heads, per = bh * s * dh;
+    std::vector<tpfuse::AttentionInputs> in;
+    for (int r = 0; r < t; ++r)
+      in.push_back(tpfuse::make_attention_inputs(batch, heads, tensor_from(q + r * per, bh, s, dh),
+                                                 tensor_from(k + r * per, bh, s, dh),
+                                                 tensor_from(v + r * per, bh, s, dh)));
+    tpfuse::AttentionOptions opt;
+    opt.scale_scores = scale != 0;
+    auto outs = tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
+      return tpfuse::fuse_all_to_all_attention(ep, in[ep.rank()], opt);
+    });
+    size_t off = 0;
+    for (auto& o : outs) {
+      copy_out(o, out + off);
+      off += o.raw().size();
+    }
+  });
+}

@@ -416,3 +416,60 @@ int or_mlp_square(int t, int kind, int m, int64_t b, int64_t s, int64_t d, int64
   free(hid); free(act_full);
   return rc;
 }
+
+/* ------------------------------------------------ UP: fused all-to-all attention */
+#include <math.h>
+/* attention_context (layers.cpp:107-118): softmax(q k^T * scale) v for one folded head,
+ * q (sq, dh), k/v (sk, dh) -> o (sq, dh). softmax_rows: max-subtracted (tensor.cpp:123-143). */
+static void attention_head(int64_t sq, int64_t sk, int64_t dh, int scale, const double* q,
+                           const double* k, const double* v, double* o, double* scores) {
+  const double sc = scale ? 1.0 / sqrt((double)dh) : 1.0;
+  for (int64_t i = 0; i < sq; ++i) {
+    double* row = scores + i * sk;
+    for (int64_t j = 0; j < sk; ++j) {
+      double acc = 0.0;
+      for (int64_t d = 0; d < dh; ++d) acc += q[i * dh + d] * k[j * dh + d];
+      row[j] = acc * sc;
+    }
+    double mx = row[0];
+    for (int64_t j = 1; j < sk; ++j) mx = row[j] > mx ? row[j] : mx;
+    double den = 0.0;
+    for (int64_t j = 0; j < sk; ++j) { row[j] = exp(row[j] - mx); den += row[j]; }
+    for (int64_t j = 0; j < sk; ++j) row[j] /= den;
+    for (int64_t d = 0; d < dh; ++d) {
+      double acc = 0.0;
+      for (int64_t j = 0; j < sk; ++j) acc += row[j] * v[j * dh + d];
+      o[i * dh + d] = acc;
+    }
+  }
+}
+
+/* fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218). Per rank r: q/k/v
+ * (batch*heads, S, dh) for its head group over the full sequence. Iteration i sends
+ * slice l = (r+i+1)%T's context to rank l (keeps its own at i = T-1); rank l assembles
+ * concat_feat over SOURCE rank of merge_heads(part): out[l] (batch, S/T, T*heads*dh),
+ * feature index (src*heads + hh)*dh + d. q/k/v: T stacked ranks; out: T stacked. */
+int or_attention_a2a(int t, int batch, int heads, int64_t s, int64_t dh, int scale,
+                     const double* q, const double* k, const double* v, double* out) {
+  if (t < 1 || batch < 1 || heads < 1 || s % t != 0) return -1;
+  const int64_t sl = s / t, bh = (int64_t)batch * heads, per = bh * s * dh;
+  const int64_t fw = (int64_t)t * heads * dh;
+  double* scores = (double*)malloc(sizeof(double) * (size_t)(sl * s));
+  double* o = (double*)malloc(sizeof(double) * (size_t)(sl * dh));
+  for (int r = 0; r < t; ++r)
+    for (int i = 0; i < t; ++i) {
+      const int l = (r + i + 1) % t;  /* send_to == slice */
+      for (int64_t g = 0; g < bh; ++g) {
+        const int64_t b = g / heads, hh = g % heads;
+        const double* qg = q + r * per + g * s * dh + (int64_t)l * sl * dh;
+        attention_head(sl, s, dh, scale, qg, k + r * per + g * s * dh, v + r * per + g * s * dh, o,
+                       scores);
+        double* dst = out + (int64_t)l * batch * sl * fw;
+        for (int64_t row = 0; row < sl; ++row)
+          for (int64_t d = 0; d < dh; ++d)
+            dst[(b * sl + row) * fw + ((int64_t)r * heads + hh) * dh + d] = o[row * dh + d];
+      }
+    }
+  free(scores); free(o);
+  return 0;
+}

@@ -74,6 +74,7 @@ _lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + 
 _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
 _lib.tpf_dp_grad_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int] * 4 + [_vp]
 _lib.tpf_dp_param_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
+_lib.tpf_attention_a2a.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
 _lib.tpf_sym_bytes_dp_ag.argtypes = [C.c_int, _i64, _i64]
 _lib.tpf_sym_bytes_dp_ag.restype = _i64
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
@@ -86,7 +87,7 @@ EXPORTED_SYMBOLS = (
     "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
     "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
     "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_dp_param_ag_gemm", "tpf_sym_bytes_dp_ag", "tpf_gemm",
+    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_attention_a2a", "tpf_dp_param_ag_gemm", "tpf_sym_bytes_dp_ag", "tpf_gemm",
     "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
 )
 
@@ -281,6 +282,18 @@ def _dp_param_ag_gemm(self, x, w_rows, out, stream=None) -> None:
 
 
 Communicator.dp_param_ag_gemm = _dp_param_ag_gemm
+
+
+def _attention_a2a(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
+    """fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218; BASELINE cfg 5).
+    Per rank q/k/v: (batch*heads, S, Dh) bf16; out: (batch, S/T, T*heads*Dh) bf16.
+    A local group takes rank-stacked tensors."""
+    S, Dh = q.shape[-2:]
+    _check(_lib.tpf_attention_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch, heads,
+                                  S, Dh, int(bool(scale)), _stream_ptr(stream)))
+
+
+Communicator.attention_a2a = _attention_a2a
 
 
 def sym_bytes_dp_ag(world, K, N_local) -> int:

@@ -9,6 +9,9 @@
 #include "tpf.h"
 #include "tpf_host.h"
 #include "tpf_internal.h"
+#include "tpf_ptx.cuh"
+
+#include <algorithm>
 
 namespace tpf {
 namespace {
@@ -53,3 +56,75 @@ extern "C" int tpf_swiglu(const void* gu, void* out, int64_t rows, int64_t F, vo
       static_cast<const uint4*>(gu), static_cast<uint4*>(out), rows, f_vec);
   return cudaGetLastError() == cudaSuccess ? TPF_OK : TPF_E_CUDA;
 }
+
+// ------------------------------------------------------------ UP attention helpers
+namespace tpf {
+namespace {
+
+// Row softmax (softmax_rows, tensor.cpp:123-143, max-subtracted) of scale * scores:
+// fp32 (rows, cols) -> bf16 P. One CTA per row, three passes over the (L2-resident) row.
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ s,
+                                                           __nv_bfloat16* __restrict__ p,
+                                                           int64_t cols, float scale_log2e) {
+  __shared__ float red[32];
+  const float* row = s + static_cast<int64_t>(blockIdx.x) * cols;
+  __nv_bfloat16* out = p + static_cast<int64_t>(blockIdx.x) * cols;
+  float mx = -INFINITY;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, row[c]);
+  for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) mx = fmaxf(mx, red[w]);
+  __syncthreads();
+  float sum = 0.f;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) sum += exp2f((row[c] - mx) * scale_log2e);
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  sum = 0.f;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) sum += red[w];
+  const float inv = 1.f / sum;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
+    out[c] = __float2bfloat16_rn(exp2f((row[c] - mx) * scale_log2e) * inv);
+}
+
+// Wait until every flag[i] >= epoch (bounded; error record on timeout).
+__global__ void wait_flags_kernel(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns,
+                                  uint32_t* err, int rank) {
+  const uint64_t t0 = globaltimer();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    while (ld_relaxed_sys(flags + i) < epoch) {
+      if (ld_relaxed_sys(err + 4)) return;
+      if (globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
+        if (atomicCAS(err, 0u, 1u) == 0u) {
+          err[1] = static_cast<uint32_t>(rank);
+          err[2] = 0xFFFFFFFFu;
+          err[3] = static_cast<uint32_t>(i);
+        }
+        atomicExch(err + 4, 1u);
+        return;
+      }
+      __nanosleep(64);
+    }
+    (void)ld_acquire_sys(flags + i);
+  }
+}
+
+}  // namespace
+
+void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st) {
+  softmax_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(s, static_cast<__nv_bfloat16*>(p), cols,
+                                                                   scale * 1.4426950408889634f);
+}
+
+void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
+                       int rank, cudaStream_t st) {
+  if (n <= 0) return;
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 64));
+  wait_flags_kernel<<<blocks, threads, 0, st>>>(flags, n, epoch, timeout_ns, err, rank);
+}
+
+}  // namespace tpf

@@ -46,6 +46,13 @@ struct KParams {
   int gather_b;        // OP_AG variant: the ring carries B (weight column blocks), not A (DP param AG)
   int64_t out_ld;      // output row stride (elements)
   int64_t blk_cols;    // gather_b: columns of one rank's weight block (output column offset unit)
+  // plain (T == 1) path extensions used by the UP attention pipeline
+  int b_batched;                      // tmap_b has a batch dim: B operand differs per batch row-block
+  int heads_merge;                    // >0: batch g -> (b = g / heads, hh = g % heads), column hh*N
+  int64_t a_row_off[kMaxRanks];       // per hosted rank: A row offset (query slice)
+  char* out_rank[kMaxRanks];          // per hosted rank: output base (may be a peer pointer)
+  int64_t out_col_off[kMaxRanks];     // per hosted rank: output column offset
+  uint32_t* done_rank[kMaxRanks];     // per hosted rank: per tile-warp completion flags (peer) or null
   int wire_f32;        // RS wire dtype: 1 fp32, 0 bf16
   int out_f32;         // output dtype: 1 fp32, 0 bf16
   int nmb_per_batch;   // ceil(Sc / BM)
@@ -91,6 +98,9 @@ enum TraceKind : int {
 };
 
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
+void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
+void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
+                       int rank, cudaStream_t st);
 int max_pairs();
 int num_sms();
 

@@ -39,7 +39,8 @@ namespace tpf {
 namespace {
 
 struct Tile {
-  int step, mb, nt, b, row0, valid;  // mb: THIS CTA's m-block; valid rows (0 if mb >= nmb)
+  int step, mb, nt, b, row0, valid;  // mb: THIS CTA's m-block; valid rows (0: dummy CTA)
+  int pair;                          // m-block pair index within the step
 };
 
 // Pair-tile raster: step-major; inside a step, group_m m-block pairs sweep the n-tiles.
@@ -52,14 +53,18 @@ __device__ __forceinline__ Tile get_tile(const KParams& p, int lin, int cta) {
   const int g0 = (rem / (GM * p.nnt)) * GM;
   const int gm = min(GM, p.npairs - g0);
   const int r2 = rem - g0 * p.nnt;
-  t.mb = 2 * (g0 + r2 % gm) + cta;
+  // Pairs never straddle a batch: the pair shares one B tile (cta_group::2), and with a
+  // per-batch B (attention heads) both CTAs must be in the same batch.
+  t.pair = g0 + r2 % gm;
   t.nt = r2 / gm;
-  if (t.mb >= p.nmb) {
-    t.b = 0; t.row0 = 0; t.valid = 0;
+  const int ppb = (p.nmb_per_batch + 1) / 2;
+  t.b = t.pair / ppb;
+  const int j = 2 * (t.pair - t.b * ppb) + cta;
+  t.mb = t.b * p.nmb_per_batch + j;
+  if (j >= p.nmb_per_batch) {
+    t.row0 = 0; t.valid = 0;
     return t;
   }
-  t.b = t.mb / p.nmb_per_batch;
-  const int j = t.mb - t.b * p.nmb_per_batch;
   t.row0 = j * BM;
   t.valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - t.row0));
   return t;
@@ -340,7 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       if (t.valid == 0)
         arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
       else if (p.op == OP_RS)
-        arow = (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
+        arow = p.a_row_off[h] +
+               (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
       else if (p.gather_b)
         arow = t.row0;
       else
@@ -353,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, rank, aslot, img0) : nullptr;
       int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
       uint64_t t_first = 0;
-      const int fwd_key = p.gather_b ? (t.mb >> 1) : t.nt;  // which tiles forward (pair / n-tile)
+      const int fwd_key = p.gather_b ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
       const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
       for (int kb = 0; kb < p.nkb; ++kb) {
         if (wire_live && kb > ready) {
@@ -406,12 +412,20 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             tma_load_2sm_5d(sb, &p.tmap_wire, fb, 0, 0, img, aslot, h);
           } else if (p.b_kmajor) {
             // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
-            tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
+            if (p.b_batched)
+              tma_load_2sm_4d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
+            else
+              tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
           } else {
 #pragma unroll
-            for (int q = 0; q < BN / 128; ++q)
-              tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
-                              kb * BK, h);
+            for (int q = 0; q < BN / 128; ++q) {
+              if (p.b_batched)
+                tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                                kb * BK, t.b, h);
+              else
+                tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                                kb * BK, h);
+            }
           }
           if (p.trace && kb == 0) t_first = globaltimer();
         }
@@ -438,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (fwd) {
           const Tile t = get_tile(p, lin, 0);
           const int it = t.step % p.T;
-          const int key = p.gather_b ? (t.mb >> 1) : t.nt;
+          const int key = p.gather_b ? t.pair : t.nt;
           if (it < p.T - 1 && key < nfwd) fwd_nt = key;
         }
         for (int kb = 0; kb < p.nkb; ++kb) {
@@ -499,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
-        const int key = p.gather_b ? (t.mb >> 1) : t.nt;
+        const int key = p.gather_b ? t.pair : t.nt;
         if (!(it < p.T - 1 && key < nfwd)) continue;
         const int slot = pass * (p.T - 1) + it;
         const int dst_rank = p.sched[rank][it][0];
@@ -647,8 +661,12 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       __syncwarp();
       char* dst_tile =
           (last || !tile_live) ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
-      const int64_t orow = static_cast<int64_t>(t.b) * p.out_rows + pass * p.Sc + t.row0 + row;
-      char* rp = out_h + orow * p.out_ld * esz;
+      // heads_merge (UP): batch g = b*heads + hh -> rows of b, columns hh*N (merge_heads fused)
+      const int hm = p.heads_merge;
+      const int64_t ob = hm ? t.b / hm : t.b;
+      const int64_t ocol = p.out_col_off[h] + (hm ? static_cast<int64_t>(t.b % hm) * p.N : 0);
+      const int64_t orow = ob * p.out_rows + pass * p.Sc + t.row0 + row;
+      char* rp = (p.out_rank[h] ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
       for (int j = 0; j < BN / 32; ++j) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + j * 32, r);
@@ -681,6 +699,12 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         pend[npend++] = flag_ptr(p, send_rank, slot_send, fidx);
         if (npend == kPend) publish();
         if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_FLAG, rank, t.step, lin, t_epi0, globaltimer());
+      }
+      if (last && tile_live && p.done_rank[h]) {
+        // completion flag for a pushed output tile (UP all-to-all)
+        fence_sys();
+        __syncwarp();
+        if (lane == 0 && rank != p.fault_rank) st_relaxed_sys(p.done_rank[h] + fidx, p.epoch);
       }
       if (p.trace && lane == 0 && ew == 0 && tile_live)
         trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -138,6 +139,8 @@ struct tpf_comm {
   int device = 0;
   int fault_rank = -1;
   int compute_only = 0;
+  char* scratch = nullptr;
+  size_t scratch_bytes = 0;
   unsigned long long* trace = nullptr;
   int64_t trace_cap = 0;
 };
@@ -156,7 +159,7 @@ Geometry geometry(int64_t B, int64_t Sc, int64_t K, int64_t N) {
   g.nmb = static_cast<int>(B) * g.nmb_per_batch;
   g.nnt = static_cast<int>(ceil_div(N, tpf::BN));
   g.nkb = static_cast<int>(ceil_div(K, tpf::BK));
-  g.npairs = (g.nmb + 1) / 2;
+  g.npairs = static_cast<int>(B) * ((g.nmb_per_batch + 1) / 2);  // pairs stay within a batch
   return g;
 }
 
@@ -172,6 +175,13 @@ struct Call {
   int b_kmajor;    // w is stored (N, K) (PyTorch Linear layout): K-major B
   int gather_b;    // AG ring carries weight column blocks (DP param all-gather)
   int64_t out_ld;  // output row stride (0: N)
+  int b_batched;   // w is per batch block: (R, B, rowsW, colsW)
+  int heads_merge;
+  int64_t a_row_off[tpf::kMaxRanks];
+  char* out_rank[tpf::kMaxRanks];
+  int64_t out_col_off[tpf::kMaxRanks];
+  uint32_t* done_rank[tpf::kMaxRanks];
+  bool no_epoch;   // do not advance the epoch (steps of one multi-launch collective)
   const void* x;
   const void* w;
   void* out;
@@ -185,7 +195,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   const Geometry g = geometry(k.B, k.Sc, k.K, NG);
   const int R = k.n_hosted;
   const int64_t x_rank_stride = k.B * k.x_rows * k.K * 2;
-  const int64_t w_rank_stride = k.K * NG * 2;
+  const int64_t w_rank_stride = k.K * NG * 2 * (k.b_batched ? k.B : 1);
   const int64_t esz = k.out_f32 ? 4 : 2;
   if (k.a_mn) {
     const uint64_t dims[4] = {static_cast<uint64_t>(k.x_rows), static_cast<uint64_t>(k.K),
@@ -207,7 +217,15 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     if (!s.good()) return s;
   }
   const int64_t out_ld = k.out_ld > 0 ? k.out_ld : k.N;
-  if (k.b_kmajor || k.gather_b) {
+  if (k.b_batched) {
+    const bool km = k.b_kmajor != 0;
+    const uint64_t d0 = km ? k.K : NG, d1 = km ? NG : k.K;
+    const uint64_t dims[4] = {d0, d1, static_cast<uint64_t>(k.B), static_cast<uint64_t>(R)};
+    const uint64_t strides[3] = {d0 * 2, d0 * d1 * 2, static_cast<uint64_t>(w_rank_stride)};
+    const uint32_t box[4] = {km ? static_cast<uint32_t>(tpf::BK) : 64u, km ? static_cast<uint32_t>(tpf::BN / 2) : static_cast<uint32_t>(tpf::BK), 1, 1};
+    tpf::Status s = make_tmap(&p.tmap_b, k.w, 4, dims, strides, box);
+    if (!s.good()) return s;
+  } else if (k.b_kmajor || k.gather_b) {
     const uint64_t dims[3] = {static_cast<uint64_t>(k.K), static_cast<uint64_t>(NG),
                               static_cast<uint64_t>(R)};
     const uint64_t strides[2] = {static_cast<uint64_t>(k.K * 2), static_cast<uint64_t>(w_rank_stride)};
@@ -235,6 +253,14 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.gather_b = k.gather_b;
   p.out_ld = out_ld;
   p.blk_cols = k.N;
+  p.b_batched = k.b_batched;
+  p.heads_merge = k.heads_merge;
+  for (int r = 0; r < tpf::kMaxRanks; ++r) {
+    p.a_row_off[r] = k.a_row_off[r];
+    p.out_rank[r] = k.out_rank[r];
+    p.out_col_off[r] = k.out_col_off[r];
+    p.done_rank[r] = k.done_rank[r];
+  }
   p.wire_f32 = k.wire_f32;
   p.out_f32 = k.out_f32;
   p.nmb_per_batch = g.nmb_per_batch;
@@ -311,7 +337,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     p.sched[0][0][0] = -1;
     p.sched[0][0][1] = -1;
     p.sched[0][0][2] = 0;
-    p.epoch = 1;
+    p.epoch = (c && k.no_epoch) ? c->epoch : 1;
   }
   p.err = c ? c->err : default_err_buffer();
   if (!p.err) return tpf::Status::cuda("no device error buffer (CUDA unavailable)");
@@ -470,6 +496,7 @@ int tpf_comm_destroy(tpf_comm* c) {
     if (c->opened[r]) cudaIpcCloseMemHandle(c->sym[r]);
   if (c->local) cudaFree(c->local);
   if (c->err) cudaFree(c->err);
+  if (c->scratch) cudaFree(c->scratch);
   delete c;
   return TPF_OK;
 }
@@ -608,6 +635,88 @@ int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* o
   }
   s = launch(c, k, static_cast<cudaStream_t>(stream));
   return s.good() ? TPF_OK : fail(s);
+}
+
+int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
+                      int64_t heads, int64_t S, int64_t Dh, int scale, void* stream_v) {
+  // fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218) on the GEMM kernel family.
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  if (batch < 1 || heads < 1 || S < 1 || Dh < 1)
+    return fail(tpf::Status::invalid("attention inputs need batch >= 1, heads >= 1"));
+  if (S % T)
+    return fail(tpf::Status::invalid("fuse_all_to_all_attention: sequence length " + std::to_string(S) +
+                                     " is not divisible by group size " + std::to_string(T)));
+  if (Dh % 8 || S % 8) return fail(tpf::Status::shape("attention: head_dim and seq must be multiples of 8"));
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const int R = hosted(c);
+  const int r0 = c->local_group ? 0 : c->rank;
+  const int64_t G = batch * heads, sl = S / T, fw = static_cast<int64_t>(T) * heads * Dh;
+  const Geometry gpv = geometry(G, sl, S, Dh);
+  const int64_t nflags = static_cast<int64_t>(gpv.nmb) * gpv.nnt * 4;  // per source rank
+  const int64_t recv_bytes = batch * sl * fw * 2;
+  if (nflags * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
+    return fail(tpf::Status::capacity("symmetric heap too small for the attention all-to-all"));
+  // scratch: scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S)
+  const size_t sc_bytes = static_cast<size_t>(R) * G * sl * S * 4, pb_bytes = sc_bytes / 2;
+  if (c->scratch_bytes < sc_bytes + pb_bytes) {
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    TPF_CUDA_TRY(cudaMalloc(&c->scratch, sc_bytes + pb_bytes));
+    c->scratch_bytes = sc_bytes + pb_bytes;
+  }
+  float* scores = reinterpret_cast<float*>(c->scratch);
+  char* probs = c->scratch + sc_bytes;
+  c->epoch += 1;
+  const uint32_t epoch = c->epoch;
+  const int par = static_cast<int>(epoch & 1u);
+  auto recv_of = [&](int rank) { return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes); };
+  auto flags_of = [&](int rank) {
+    return reinterpret_cast<uint32_t*>(c->sym[rank] + par * kFlagBytesPerParity);
+  };
+  for (int i = 0; i < T; ++i) {
+    // 1) scores = Q[slice l] K^T for every head (K-major B = K itself, batched per head)
+    Call qk{};
+    qk.op = tpf::OP_RS; qk.T = 1; qk.m = 1; qk.out_f32 = 1; qk.n_hosted = R; qk.rank0 = r0;
+    qk.B = G; qk.Sc = sl; qk.K = Dh; qk.N = S; qk.x_rows = S; qk.out_rows = sl;
+    qk.x = q; qk.w = k; qk.out = scores; qk.b_kmajor = 1; qk.b_batched = 1; qk.no_epoch = true;
+    for (int h = 0; h < R; ++h) qk.a_row_off[h] = static_cast<int64_t>((r0 + h + i + 1) % T) * sl;
+    s = launch(c, qk, stream);
+    if (!s.good()) return fail(s);
+    // 2) P = softmax(scale * scores) rows
+    tpf::launch_softmax(scores, probs, static_cast<int64_t>(R) * G * sl, S,
+                        scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f, stream);
+    // 3) O = P V, epilogue pushes each tile to the slice owner's receive buffer at the
+    //    source rank's feature block (merge_heads + concat_feat fused) and flags it.
+    Call pv{};
+    pv.op = tpf::OP_RS; pv.T = 1; pv.m = 1; pv.out_f32 = 0; pv.n_hosted = R; pv.rank0 = r0;
+    pv.B = G; pv.Sc = sl; pv.K = S; pv.N = Dh; pv.x_rows = sl; pv.out_rows = sl;
+    pv.x = probs; pv.w = v; pv.out = out; pv.b_batched = 1; pv.heads_merge = static_cast<int>(heads);
+    pv.out_ld = fw; pv.no_epoch = true;
+    for (int h = 0; h < R; ++h) {
+      const int rank = r0 + h, dst = (rank + i + 1) % T;
+      pv.out_rank[h] = recv_of(dst);
+      pv.out_col_off[h] = static_cast<int64_t>(rank) * heads * Dh;
+      pv.done_rank[h] = dst == rank ? nullptr : flags_of(dst) + rank * nflags;
+    }
+    s = launch(c, pv, stream);
+    if (!s.good()) return fail(s);
+  }
+  // 4) wait for the T-1 incoming parts (flags are indexed by source rank; the own part
+  //    was written locally in the last step), then hand the assembled slice to the caller.
+  for (int h = 0; h < R; ++h) {
+    const int rank = r0 + h;
+    uint32_t* f = flags_of(rank);
+    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags, epoch, c->timeout_ns, c->err, rank, stream);
+    tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags, static_cast<int64_t>(T - 1 - rank) * nflags,
+                           epoch, c->timeout_ns, c->err, rank, stream);
+    TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + h * recv_bytes, recv_of(rank), recv_bytes,
+                                 cudaMemcpyDeviceToDevice, stream));
+  }
+  TPF_CUDA_TRY(cudaGetLastError());
+  return TPF_OK;
 }
 
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

@@ -56,6 +56,7 @@ class Oracle:
         L.or_row_parallel.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D]
         L.or_fuse_rs_identity.argtypes = [C.c_int] * 3 + [_i64] * 3 + [_D, _D]
         L.or_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
+        L.or_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
         self.L = L
 
     @staticmethod
@@ -133,6 +134,16 @@ class Oracle:
         return out.reshape(t, b, s // t, d)
 
 
+    def attention_a2a(self, t, batch, heads, q, k, v, scale=True):
+        """q/k/v: (T, batch*heads, S, dh) -> (T, batch, S/T, T*heads*dh)."""
+        _, bh, s, dh = q.shape
+        out = np.empty(t * batch * (s // t) * t * heads * dh, np.float64)
+        self._chk(self.L.or_attention_a2a(t, batch, heads, s, dh, int(scale), np.ascontiguousarray(q).reshape(-1),
+                                          np.ascontiguousarray(k).reshape(-1), np.ascontiguousarray(v).reshape(-1),
+                                          out), "fuse_all_to_all_attention: invalid arguments")
+        return out.reshape(t, batch, s // t, t * heads * dh)
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_SO)
 
@@ -152,6 +163,7 @@ class Reference:
         L.ref_fuse_rs_identity.argtypes = [C.c_int] * 3 + [_i64] * 3 + [_D, _D]
         L.ref_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
         L.ref_time_ops.argtypes = [C.c_int] + [_i64] * 6 + [C.c_int, _D, _D]
+        L.ref_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
         self.L = L
 
     def _chk(self, rc):
@@ -209,6 +221,14 @@ class Reference:
                                         np.ascontiguousarray(up).reshape(-1),
                                         np.ascontiguousarray(down).reshape(-1), out))
         return out.reshape(t, b, s // t, d)
+
+    def attention_a2a(self, t, batch, heads, q, k, v, scale=True):
+        _, bh, s, dh = q.shape
+        out = np.empty(t * batch * (s // t) * t * heads * dh, np.float64)
+        self._chk(self.L.ref_attention_a2a(t, batch, heads, s, dh, int(scale), np.ascontiguousarray(q).reshape(-1),
+                                           np.ascontiguousarray(k).reshape(-1), np.ascontiguousarray(v).reshape(-1),
+                                           out))
+        return out.reshape(t, batch, s // t, t * heads * dh)
 
     def time_ops(self, t, b, s, k_ag, n_ag, k_rs, n_rs, reps=1):
         """Per-repetition wall seconds of the reference's AG-GEMM and GEMM-RS."""

@@ -505,3 +505,44 @@ def test_dp_param_ag_gemm_full_size():
     ref32 = x[0].float() @ W.float().T
     assert (out[0].float() - ref32).abs().max().item() <= 2e-2 * ref32.abs().max().item()
     one.close()
+
+
+
+# --------------------------------------------- UP: fused all-to-all attention (a18)
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+def test_attention_a2a_vs_oracle(T):
+    """fuse_all_to_all_attention (Alg. 5): every rank ends with query slice r of all heads,
+    feature blocks ordered by source rank (concat_feat of merge_heads). Tolerance: P is
+    carried in bf16 -> rel_deviation <= 2e-2 vs the fp64 oracle on bf16-rounded inputs."""
+    batch, heads, S, Dh = 2, 2, 64 * T, 64
+    rng = np.random.default_rng(500 + T)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, (T, batch * heads, S, Dh))) for _ in range(3))
+    want = O.attention_a2a(T, batch, heads, q, k, v, True)
+    dq, dk, dv = (bf16(a).to(DEV) for a in (q, k, v))
+    out = torch.full((T, batch, S // T, T * heads * Dh), float("nan"), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, 1 << 26)
+    for _ in range(2):  # epoch / parity reuse
+        comm.attention_a2a(dq, dk, dv, out, batch, heads)
+        comm.sync()
+        got = out.double().cpu().numpy()
+        assert np.isfinite(got).all()
+        assert rel_deviation(got, want) <= 2e-2
+    comm.close()
+
+
+def test_attention_a2a_long_sequence_vs_sdpa():
+    """cfg 5 structure at S=8192, T=8, 4 heads x 128 per rank: vs torch SDPA (fp32 math)."""
+    T, batch, heads, S, Dh = 8, 1, 4, 8192, 128
+    g = torch.Generator(device=DEV).manual_seed(9)
+    q, k, v = (torch.randn((T, batch * heads, S, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3))
+    out = torch.empty((T, batch, S // T, T * heads * Dh), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, 1 << 26)
+    comm.attention_a2a(q, k, v, out, batch, heads)
+    comm.sync()
+    comm.close()
+    for r in (0, 7):
+        qs = q[:, :, r * (S // T):(r + 1) * (S // T)].float()  # every source rank's heads, slice r
+        ref = torch.nn.functional.scaled_dot_product_attention(qs, k.float(), v.float())  # (T, heads, S/T, Dh)
+        ref = ref.permute(2, 0, 1, 3).reshape(S // T, T * heads * Dh)
+        err = (out[r, 0].float() - ref).abs().max().item()
+        assert err <= 2e-2 * ref.abs().max().item() + 1e-3, (r, err)

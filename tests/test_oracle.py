@@ -164,3 +164,17 @@ def test_reference_rejections_match():
             R.row_parallel(*args, x, w)
         with pytest.raises(OracleError):
             O.row_parallel(*args, x, w)
+
+
+@needs_ref
+@pytest.mark.parametrize("t", [1, 2, 4])
+def test_attention_a2a_restatement_bitexact(t):
+    """UP (Alg. 5, fuse_all_to_all_attention): restatement == compiled reference."""
+    R = Reference()
+    rng = np.random.default_rng(40 + t)
+    for heads in (1, 2):
+        b, s, dh = 2, 8 * t, 4
+        q, k, v = (rng.uniform(-1, 1, (t, b * heads, s, dh)) for _ in range(3))
+        for scale in (True, False):
+            assert np.array_equal(O.attention_a2a(t, b, heads, q, k, v, scale),
+                                  R.attention_a2a(t, b, heads, q, k, v, scale))
