@@ -20,6 +20,15 @@ constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 512;  // + barriers
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
 enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };
+// Kernel instance (compile-time operand layout / epilogue variant).
+enum Mode : int {
+  MODE_STD = 0,       // A K-major (x rows), B MN-major (W (K, N)): TP AG-GEMM / GEMM-RS / GEMM
+  MODE_DP_GRAD = 1,   // GEMM-RS with A MN-major (X^T from row-major X): DP gradient RS
+  MODE_GATHER_B = 2,  // AG carrying B (K-major W rows): DP parameter all-gather
+  MODE_QK = 3,        // B K-major, per batch (head); per-rank A row offset: UP scores
+  MODE_PV = 4,        // B MN-major, per batch; merge_heads + peer push + flags: UP output
+  MODE_SINGLE = 5,    // MODE_STD operands, T == 1 (no ring): the degenerate GEMM (+ epilogue act)
+};
 
 // Error record in device memory (first error wins).
 //   [0] code (0 ok, 1 peer-flag timeout, 2 mbarrier timeout)
@@ -31,6 +40,7 @@ struct KParams {
   CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); b_kmajor: (K, N, ranks)
   CUtensorMap tmap_wire;  // AG wire images (128 B, 128 rows, image, slot, hosted rank), no swizzle
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
+  int mode;            // Mode (kernel instance)
   int T;               // group size
   int m;               // granularity (ring passes)
   int direct;          // 1: pairwise rs_direct fold; 0: pipelined (ring / circular)

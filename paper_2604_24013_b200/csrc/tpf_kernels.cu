@@ -271,7 +271,16 @@ __device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0,
 
 }  // namespace
 
+// Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
+// single-thread producer / MMA loops cost measurable throughput.
+template <int kOp, int kMode>
 __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_constant__ KParams p) {
+  constexpr bool kAMn = kMode == MODE_DP_GRAD;                         // A MN-major (X^T)
+  constexpr bool kGatherB = kMode == MODE_GATHER_B;                    // AG carries B
+  constexpr bool kBBatched = kMode == MODE_QK || kMode == MODE_PV;     // B per batch (head)
+  constexpr bool kBKMajor = kGatherB || kMode == MODE_QK;              // B stored (N, K)
+  constexpr bool kUpEpi = kMode == MODE_PV;                            // merge_heads + push + flags
+  constexpr bool kSingle = kMode == MODE_SINGLE;                       // T == 1: no ring at all
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -300,14 +309,14 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   const bool active = h < p.n_hosted;  // (grid is sized exactly; kept for safety)
   // AG ring forwarding rides the A pipeline: the stage image is bulk-stored to the
   // successor before the stage is recycled (so `empty` also waits for the forwarder).
-  const bool fwd = p.op == OP_AG && p.T > 1 && !p.compute_only;
+  const bool fwd = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
   const int nfwd = min(p.ag_nfwd, p.nnt);       // leading n-tiles that forward an m-block
   const int fbatch = min(max(p.ag_batch, 1), 16);  // forwards per fence + flag publication
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tmap_a);
     prefetch_tmap(&p.tmap_b);
-    if (p.op == OP_AG && p.T > 1) prefetch_tmap(&p.tmap_wire);
+    if (kOp == OP_AG && p.T > 1) prefetch_tmap(&p.tmap_wire);
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -331,35 +340,36 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (!active) {
   } else if (warp == 0) {
     // ===================================================== TMA producer (both CTAs)
-    // The whole warp walks the schedule (the wire-image flag scan is warp-parallel);
-    // lane 0 issues barrier arrivals and TMA loads.
+    // With AG wire inputs the whole warp walks the schedule (the wire-image flag scan is
+    // warp-parallel); otherwise lane 0 alone. Lane 0 issues barrier arrivals and TMA loads.
+    const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
     int stage = 0;
     uint32_t phase = 0;
-    for (int lin = gp; lin < ntiles; lin += GP) {
+    for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
       const Tile t = get_tile(p, lin, cta);
       const int pass = t.step / p.T, it = t.step - pass * p.T;
-      const bool from_wire = (p.op == OP_AG) && it > 0 && !p.compute_only;
-      const bool a_from_wire = from_wire && !p.gather_b;
-      const bool b_from_wire = from_wire && p.gather_b;
+      const bool from_wire = !kSingle && (kOp == OP_AG) && it > 0 && !p.compute_only;
+      const bool a_from_wire = from_wire && !kGatherB;
+      const bool b_from_wire = from_wire && kGatherB;
       int64_t arow;
       if (t.valid == 0)
         arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
-      else if (p.op == OP_RS)
-        arow = p.a_row_off[h] +
+      else if (kOp == OP_RS)
+        arow = (kMode == MODE_QK ? p.a_row_off[h] : 0) +
                (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
-      else if (p.gather_b)
+      else if (kGatherB)
         arow = t.row0;
       else
         arow = pass * p.Sc + t.row0;
       const int aslot = pass * (p.T - 1) + it - 1;
       // wire images of this CTA's operand for this tile: A rows (m-block) or B half (n-tile)
-      const int64_t img0 = p.gather_b ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
+      const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
                                       : static_cast<int64_t>(t.mb) * p.nkb;
       const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
       const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, rank, aslot, img0) : nullptr;
       int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
       uint64_t t_first = 0;
-      const int fwd_key = p.gather_b ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
+      const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
       const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
       for (int kb = 0; kb < p.nkb; ++kb) {
         if (wire_live && kb > ready) {
@@ -399,7 +409,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             mbar_arrive_cluster(fb);
           if (a_from_wire) {
             tma_load_2sm_5d(sa, &p.tmap_wire, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
-          } else if (p.a_mn) {
+          } else if (kAMn) {
             // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
 #pragma unroll
             for (int q = 0; q < BM / 64; ++q)
@@ -410,16 +420,16 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           }
           if (b_from_wire) {
             tma_load_2sm_5d(sb, &p.tmap_wire, fb, 0, 0, img, aslot, h);
-          } else if (p.b_kmajor) {
+          } else if (kBKMajor) {
             // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
-            if (p.b_batched)
+            if (kBBatched)
               tma_load_2sm_4d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
             else
               tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
           } else {
 #pragma unroll
             for (int q = 0; q < BN / 128; ++q) {
-              if (p.b_batched)
+              if (kBBatched)
                 tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                                 kb * BK, t.b, h);
               else
@@ -437,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     // ===================================================== MMA issuer (leader CTA)
     if (leader && lane == 0) {
       const uint32_t idesc =
-          make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/p.b_kmajor == 0 && p.gather_b == 0, /*a_mn_major=*/p.a_mn != 0);
+          make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/!kBKMajor, /*a_mn_major=*/kAMn);
       int stage = 0;
       uint32_t phase = 0;
       int lt = 0;
@@ -452,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (fwd) {
           const Tile t = get_tile(p, lin, 0);
           const int it = t.step % p.T;
-          const int key = p.gather_b ? t.pair : t.nt;
+          const int key = kGatherB ? t.pair : t.nt;
           if (it < p.T - 1 && key < nfwd) fwd_nt = key;
         }
         for (int kb = 0; kb < p.nkb; ++kb) {
@@ -470,11 +480,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           for (int k = 0; k < BK / 16; ++k) {
             // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
             // MN-major A: like B, 16 K-rows = 2048 B, LBO = 64-row atom (8 KiB), SBO = 1 KiB.
-            const uint64_t ad = p.a_mn ? make_sdesc(abase + k * 2048, 64 * BK * 2, 1024)
+            const uint64_t ad = kAMn ? make_sdesc(abase + k * 2048, 64 * BK * 2, 1024)
                                        : make_sdesc(abase + k * 32, 0, 1024);
             // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
             // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
-            const uint64_t bd = (p.b_kmajor || p.gather_b) ? make_sdesc(bbase + k * 32, 0, 1024)
+            const uint64_t bd = kBKMajor ? make_sdesc(bbase + k * 32, 0, 1024)
                                                            : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
             mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
           }
@@ -513,16 +523,16 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
-        const int key = p.gather_b ? t.pair : t.nt;
+        const int key = kGatherB ? t.pair : t.nt;
         if (!(it < p.T - 1 && key < nfwd)) continue;
         const int slot = pass * (p.T - 1) + it;
         const int dst_rank = p.sched[rank][it][0];
         const uint64_t t0 = p.trace ? globaltimer() : 0;
         // forwarded operand: this CTA's A rows, or (gather_b) its half of the B tile
-        const bool live = p.gather_b ? true : t.valid > 0;
-        const int64_t img0 = p.gather_b ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
+        const bool live = kGatherB ? true : t.valid > 0;
+        const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
                                         : static_cast<int64_t>(t.mb) * p.nkb;
-        const uint8_t* sbase = p.gather_b ? smem_b : smem_a;
+        const uint8_t* sbase = kGatherB ? smem_b : smem_a;
         for (int kb = key; kb < p.nkb; kb += nfwd) {
           const bool mine = ((fo / fbatch) & 1) == grp;
           const bool batch_end = (fo % fbatch) == fbatch - 1;
@@ -591,13 +601,13 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const int64_t tile_idx = static_cast<int64_t>(t.mb) * p.nnt + t.nt;
       const int64_t fidx = tile_idx * 4 + ew;
 
-      if (p.op == OP_AG) {
+      if (kOp == OP_AG) {
         const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
         // gather_b: rows stay local, the step selects the output column block l
-        const int64_t orow = p.gather_b ? static_cast<int64_t>(t.b) * p.out_rows + t.row0 + row
+        const int64_t orow = kGatherB ? static_cast<int64_t>(t.b) * p.out_rows + t.row0 + row
                                         : static_cast<int64_t>(t.b) * p.out_rows +
                                               (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
-        char* rp = out_h + (orow * p.out_ld + (p.gather_b ? static_cast<int64_t>(l) * p.blk_cols : 0)) * esz;
+        char* rp = out_h + (orow * p.out_ld + (kGatherB ? static_cast<int64_t>(l) * p.blk_cols : 0)) * esz;
         if (p.act == ACT_SWIGLU) {
           // Tile-interleaved W: columns [0,128) of the tile are gate, [128,256) the matching
           // up columns -> 128 output columns silu(gate) * up (Llama MLP, fused).
@@ -662,11 +672,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       char* dst_tile =
           (last || !tile_live) ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
       // heads_merge (UP): batch g = b*heads + hh -> rows of b, columns hh*N (merge_heads fused)
-      const int hm = p.heads_merge;
+      const int hm = kUpEpi ? p.heads_merge : 0;
       const int64_t ob = hm ? t.b / hm : t.b;
-      const int64_t ocol = p.out_col_off[h] + (hm ? static_cast<int64_t>(t.b % hm) * p.N : 0);
+      const int64_t ocol = kUpEpi ? p.out_col_off[h] + (hm ? static_cast<int64_t>(t.b % hm) * p.N : 0) : 0;
       const int64_t orow = ob * p.out_rows + pass * p.Sc + t.row0 + row;
-      char* rp = (p.out_rank[h] ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
+      char* rp = ((kUpEpi && p.out_rank[h]) ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
       for (int j = 0; j < BN / 32; ++j) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + j * 32, r);
@@ -700,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (npend == kPend) publish();
         if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_FLAG, rank, t.step, lin, t_epi0, globaltimer());
       }
-      if (last && tile_live && p.done_rank[h]) {
+      if (kUpEpi && last && tile_live && p.done_rank[h]) {
         // completion flag for a pushed output tile (UP all-to-all)
         fence_sys();
         __syncwarp();
@@ -718,11 +728,13 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (warp == 2) tmem_dealloc_2sm<512>(tmem_base);
 }
 
-void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
+namespace {
+
+template <int kOp, int kMode>
+void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tpf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSmemBytes);
+    cudaFuncSetAttribute(tpf_fused_kernel<kOp, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr_set = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -737,15 +749,33 @@ void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, tpf_fused_kernel, p);
+  cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, p);
+}
+
+}  // namespace
+
+void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
+  switch (p.mode) {
+    case MODE_DP_GRAD: launch_instance<OP_RS, MODE_DP_GRAD>(p, grid, stream); return;
+    case MODE_GATHER_B: launch_instance<OP_AG, MODE_GATHER_B>(p, grid, stream); return;
+    case MODE_QK: launch_instance<OP_RS, MODE_QK>(p, grid, stream); return;
+    case MODE_PV: launch_instance<OP_RS, MODE_PV>(p, grid, stream); return;
+    case MODE_SINGLE:
+      if (p.op == OP_AG) launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream);
+      else launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);
+      return;
+    default:
+      if (p.op == OP_AG) launch_instance<OP_AG, MODE_STD>(p, grid, stream);
+      else launch_instance<OP_RS, MODE_STD>(p, grid, stream);
+  }
 }
 
 // Largest number of co-resident CTA pairs (all CTAs must be resident: spins on
-// other CTAs' progress rely on it).
+// other CTAs' progress rely on it). All instances share block size and smem.
 int max_pairs() {
   static int cached = -1;
   if (cached >= 0) return cached;
-  cudaFuncSetAttribute(tpf_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  cudaFuncSetAttribute(tpf_fused_kernel<OP_RS, MODE_STD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2);
   cfg.blockDim = dim3(kThreads);
@@ -758,7 +788,7 @@ int max_pairs() {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, tpf_fused_kernel, &cfg) != cudaSuccess) n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, tpf_fused_kernel<OP_RS, MODE_STD>, &cfg) != cudaSuccess) n = 0;
   cached = n;
   return n;
 }

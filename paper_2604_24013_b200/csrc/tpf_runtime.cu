@@ -242,6 +242,14 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     if (!s.good()) return s;
   }
   p.op = k.op;
+  p.mode = k.a_mn ? tpf::MODE_DP_GRAD
+         : k.gather_b ? tpf::MODE_GATHER_B
+         : (k.b_batched && k.b_kmajor) ? tpf::MODE_QK
+         : k.b_batched ? tpf::MODE_PV
+         : k.T == 1 ? tpf::MODE_SINGLE
+         : tpf::MODE_STD;
+  if ((p.mode == tpf::MODE_STD || p.mode == tpf::MODE_SINGLE) && k.b_kmajor)
+    return tpf::Status::invalid("internal: K-major B is only instantiated for the DP / UP modes");
   p.T = k.T;
   p.m = k.m;
   p.direct = k.direct;
