@@ -73,6 +73,13 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.samples.append((time.time(), line.strip()))
 
+    def wait_ready(self, timeout=5.0):
+        """Block until nvidia-smi has produced its first sample (its start-up takes
+        ~0.1-0.5 s), so the timed region that follows is actually sampled."""
+        t_end = time.time() + timeout
+        while self.proc and not self.samples and time.time() < t_end:
+            time.sleep(0.01)
+
     def mark_start(self):
         self.t0 = time.time()
 
@@ -207,6 +214,10 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- timed region (device-resident inputs); per-kernel events on the launch stream
     sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.wait_ready()
+        for _ in range(max(3, args.warmup)):  # keep the GPU busy while sampling settles
+            ag(); rs()
     n = args.steps
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
     barrier()
@@ -471,7 +482,7 @@ def emulated_block(args, dev, stream, T):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--emulate-tp", type=int, default=8, help="single-GPU local-group TP (N=1 only; 0 = off)")
