@@ -107,7 +107,23 @@ enum TraceKind : int {
   TR_FLUSH = 7,      // index = #flags; AG forwarder fence + flag publication (t1-t0)
 };
 
+// UP v2: fused flash-attention + output all-to-all (csrc/tpf_attention.cu)
+struct FmhaParams {
+  CUtensorMap tmap_q, tmap_k, tmap_v;  // (Dh = 128, S, G, hosted ranks), box (64, 128), SW128
+  int T, R, rank0, heads, G, nqt, nkv, ctas_per_rank;
+  int64_t S, sl, fw;                   // fw = T * heads * Dh (output row stride, elements)
+  float scale_log2;                    // softmax scale * log2(e)
+  char* recv[kMaxRanks];               // every rank's receive buffer (peer-mapped)
+  uint32_t* flags[kMaxRanks];          // every rank's flag block (peer-mapped)
+  int64_t nflags_per_src;              // G * nqt * 4
+  uint32_t epoch;
+  int fault_rank;
+  uint32_t* err;
+  int64_t timeout_ns;
+};
+
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
+void launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
 void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
                        int rank, cudaStream_t st);

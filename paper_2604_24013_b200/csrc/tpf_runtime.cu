@@ -666,7 +666,61 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   const int64_t recv_bytes = batch * sl * fw * 2;
   if (nflags * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
     return fail(tpf::Status::capacity("symmetric heap too small for the attention all-to-all"));
-  // scratch: scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S)
+  auto recv_at = [&](int rank, int par) {
+    return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes);
+  };
+  auto flags_at = [&](int rank, int par) {
+    return reinterpret_cast<uint32_t*>(c->sym[rank] + par * kFlagBytesPerParity);
+  };
+  if (Dh == 128 && sl % 128 == 0) {
+    // v2: one persistent fused flash-attention launch for all steps / heads / hosted ranks
+    tpf::FmhaParams fp;
+    std::memset(&fp, 0, sizeof(fp));
+    const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
+                              static_cast<uint64_t>(R)};
+    const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2),
+                                 static_cast<uint64_t>(G * S * Dh * 2)};
+    const uint32_t box[4] = {64, 128, 1, 1};
+    s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
+    if (!s.good()) return fail(s);
+    const int64_t nflags2 = G * (sl / 128) * 4;
+    if (nflags2 * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
+      return fail(tpf::Status::capacity("symmetric heap too small for the attention all-to-all"));
+    c->epoch += 1;
+    const uint32_t epoch = c->epoch;
+    const int par = static_cast<int>(epoch & 1u);
+    fp.T = T; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
+    fp.nqt = static_cast<int>(sl / 128); fp.nkv = static_cast<int>(S / 128);
+    fp.S = S; fp.sl = sl; fp.fw = fw;
+    fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
+    for (int x = 0; x < T; ++x) {
+      fp.recv[x] = recv_at(x, par);
+      fp.flags[x] = flags_at(x, par);
+    }
+    fp.nflags_per_src = nflags2;
+    fp.epoch = epoch;
+    fp.fault_rank = c->fault_rank;
+    fp.err = c->err;
+    fp.timeout_ns = c->timeout_ns;
+    const int sms = tpf::num_sms();
+    fp.ctas_per_rank = std::max(1, sms / R);
+    tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
+    TPF_CUDA_TRY(cudaGetLastError());
+    for (int hh = 0; hh < R; ++hh) {
+      const int rank = r0 + hh;
+      uint32_t* f = flags_at(rank, par);
+      tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags2, epoch, c->timeout_ns, c->err, rank, stream);
+      tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags2, static_cast<int64_t>(T - 1 - rank) * nflags2,
+                             epoch, c->timeout_ns, c->err, rank, stream);
+      TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank, par), recv_bytes,
+                                   cudaMemcpyDeviceToDevice, stream));
+    }
+    TPF_CUDA_TRY(cudaGetLastError());
+    return TPF_OK;
+  }
+  // v1 (any head_dim): scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S)
   const size_t sc_bytes = static_cast<size_t>(R) * G * sl * S * 4, pb_bytes = sc_bytes / 2;
   if (c->scratch_bytes < sc_bytes + pb_bytes) {
     if (c->scratch) cudaFree(c->scratch);

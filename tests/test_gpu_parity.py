@@ -546,3 +546,23 @@ def test_attention_a2a_long_sequence_vs_sdpa():
         ref = ref.permute(2, 0, 1, 3).reshape(S // T, T * heads * Dh)
         err = (out[r, 0].float() - ref).abs().max().item()
         assert err <= 2e-2 * ref.abs().max().item() + 1e-3, (r, err)
+
+
+@pytest.mark.parametrize("T", [1, 2, 4])
+def test_attention_a2a_fused_fmha_vs_oracle(T):
+    """UP v2 (head_dim 128: one fused tcgen05 flash-attention launch whose epilogue pushes
+    O tiles to the slice owner) vs the fp64 oracle of fuse_all_to_all_attention."""
+    batch, heads, S, Dh = 2, 2, 256 * T, 128
+    rng = np.random.default_rng(700 + T)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, (T, batch * heads, S, Dh))) for _ in range(3))
+    want = O.attention_a2a(T, batch, heads, q, k, v, True)
+    dq, dk, dv = (bf16(a).to(DEV) for a in (q, k, v))
+    out = torch.full((T, batch, S // T, T * heads * Dh), float("nan"), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, 1 << 26)
+    for _ in range(2):
+        comm.attention_a2a(dq, dk, dv, out, batch, heads)
+        comm.sync()
+        got = out.double().cpu().numpy()
+        assert np.isfinite(got).all()
+        assert rel_deviation(got, want) <= 2e-2
+    comm.close()
