@@ -184,6 +184,20 @@ int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local);
 int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                       int64_t heads, int64_t S, int64_t Dh, int scale, void* stream);
 
+/* Query-split attention (Alg. 4). Replaces:
+ *   Tensor query_split_attention(RankEndpoint&, const AttentionInputs&, const ShardedLinear& out_proj,
+ *                                const Schedule&, const AttentionOptions&)  (layers.hpp:88-91,
+ *       layers.cpp:149-172)
+ * = fuse_reduce_scatter over the query sequence of f(slice) = merge_heads(attention(q_slice, k, v)) . W_o[r].
+ *   q, k, v : bf16 (batch*heads, S, 128)  this rank's head group, full sequence
+ *   w_o     : bf16 (heads*128, D)         this rank's row shard of the output projection
+ *   out     : (batch, S/T, D) out_dtype
+ * The attention context of every slice comes from one fused tcgen05 flash-attention launch;
+ * the projection + reduce-scatter is the fused GEMM-RS (schedule reduction order). */
+int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const void* v, const void* w_o,
+                              void* out, int64_t batch, int64_t heads, int64_t S, int64_t Dh, int64_t D, int kind,
+                              int wire_dtype, int out_dtype, int scale, void* stream);
+
 /* T == 1 degenerate case of both ops (collectives.cpp:242,379): out = a * b.
  *   a: bf16 (M, K), b: bf16 (K, N), out: (M, N) out_dtype. No communicator. */
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

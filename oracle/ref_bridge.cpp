@@ -260,3 +260,29 @@ extern "C" int ref_attention_a2a(int t, int batch, int heads, int64_t s, int64_t
     }
   });
 }
+
+extern "C" int ref_query_split_attention(int t, int kind, int batch, int heads, int64_t s, int64_t dh,
+                                         int64_t d, int scale, const double* q, const double* k,
+                                         const double* v, const double* w_o, double* out) {
+  return guarded([&] {
+    const int64_t bh = static_cast<int64_t>(batch) * heads, per = bh * s * dh;
+    std::vector<tpfuse::AttentionInputs> in;
+    for (int r = 0; r < t; ++r)
+      in.push_back(tpfuse::make_attention_inputs(batch, heads, tensor_from(q + r * per, bh, s, dh),
+                                                 tensor_from(k + r * per, bh, s, dh),
+                                                 tensor_from(v + r * per, bh, s, dh)));
+    const tpfuse::ShardedLinear wo =
+        tpfuse::ShardedLinear::split_rows(matrix_from(w_o, static_cast<int64_t>(t) * heads * dh, d), t);
+    const tpfuse::Schedule sched = tpfuse::build_schedule(kind_of(kind), t);
+    tpfuse::AttentionOptions opt;
+    opt.scale_scores = scale != 0;
+    auto outs = tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
+      return tpfuse::query_split_attention(ep, in[ep.rank()], wo, sched, opt);
+    });
+    size_t off = 0;
+    for (auto& o : outs) {
+      copy_out(o, out + off);
+      off += o.raw().size();
+    }
+  });
+}

@@ -29,6 +29,7 @@
  * exactly, so it is bit-exact with the reference even on
  * non-integer fp64 data.
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -472,4 +473,43 @@ int or_attention_a2a(int t, int batch, int heads, int64_t s, int64_t dh, int sca
     }
   free(scores); free(o);
   return 0;
+}
+
+/* query_split_attention (Alg. 4, layers.cpp:149-172): fuse_reduce_scatter over the query
+ * sequence with f(q_slice) = matmul(merge_heads(attention_context(q_slice, k, v)), W_o[r]).
+ * q/k/v: T stacked ranks of (batch*heads, S, dh); w_o: (T*heads*dh, d) row-sharded by rank
+ * (row block r = this rank's head group). out: T stacked (batch, S/T, d). */
+int or_query_split_attention(int t, int kind, int batch, int heads, int64_t s, int64_t dh, int64_t d,
+                             int scale, const double* q, const double* k, const double* v,
+                             const double* w_o, double* out) {
+  if (rs_checks(t, kind, 1, s)) return -1;
+  const int64_t bh = (int64_t)batch * heads, per = bh * s * dh, hd = (int64_t)heads * dh;
+  const int64_t piece = s / t, ce = (int64_t)batch * piece * d;
+  int32_t* sched = NULL;
+  if (t > 1) {
+    sched = (int32_t*)malloc(sizeof(int32_t) * (size_t)(t * t * 3));
+    if (or_build_schedule(kind, t, sched)) { free(sched); return -1; }
+  }
+  double* parts = (double*)malloc(sizeof(double) * (size_t)(t * t * ce));
+  double* scores = (double*)malloc(sizeof(double) * (size_t)(piece * s));
+  double* o = (double*)malloc(sizeof(double) * (size_t)(piece * dh));
+  double* ctx = (double*)malloc(sizeof(double) * (size_t)(batch * piece * hd));
+  for (int r = 0; r < t; ++r) {
+    const double* wr = w_o + (int64_t)r * hd * d;
+    for (int c = 0; c < t; ++c) {
+      for (int64_t g = 0; g < bh; ++g) {
+        const int64_t b = g / heads, hh = g % heads;
+        attention_head(piece, s, dh, scale, q + r * per + g * s * dh + (int64_t)c * piece * dh,
+                       k + r * per + g * s * dh, v + r * per + g * s * dh, o, scores);
+        for (int64_t row = 0; row < piece; ++row)
+          for (int64_t e = 0; e < dh; ++e) ctx[(b * piece + row) * hd + hh * dh + e] = o[row * dh + e];
+      }
+      or_matmul(batch * piece, hd, d, ctx, wr, parts + ((int64_t)r * t + c) * ce);
+    }
+  }
+  int rc = 0;
+  if (t == 1) memcpy(out, parts, sizeof(double) * (size_t)ce);
+  else rc = fuse_rs_from_partials(t, kind, 1, batch, s, d, sched, parts, out);
+  free(sched); free(parts); free(scores); free(o); free(ctx);
+  return rc;
 }

@@ -75,6 +75,7 @@ _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
 _lib.tpf_dp_grad_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int] * 4 + [_vp]
 _lib.tpf_dp_param_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
 _lib.tpf_attention_a2a.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
+_lib.tpf_query_split_attention.argtypes = [_vp] * 6 + [_i64] * 5 + [C.c_int] * 4 + [_vp]
 _lib.tpf_sym_bytes_dp_ag.argtypes = [C.c_int, _i64, _i64]
 _lib.tpf_sym_bytes_dp_ag.restype = _i64
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
@@ -84,11 +85,35 @@ _lib.tpf_sym_bytes_rs.argtypes = [C.c_int] + [_i64] * 4 + [C.c_int, C.c_int]
 _lib.tpf_sym_bytes_rs.restype = _i64
 
 EXPORTED_SYMBOLS = (
-    "tpf_version", "tpf_last_error", "tpf_device_sms", "tpf_ring_indices", "tpf_schedule_build",
-    "tpf_schedule_check", "tpf_comm_create", "tpf_comm_ipc_handle", "tpf_comm_open_peers",
-    "tpf_comm_create_local_group", "tpf_comm_destroy", "tpf_comm_rank", "tpf_comm_world",
-    "tpf_comm_sync", "tpf_comm_set_timeout_ns", "tpf_comm_inject_fault", "tpf_comm_set_compute_only", "tpf_comm_set_trace", "tpf_ag_gemm", "tpf_gemm_rs", "tpf_dp_grad_rs", "tpf_attention_a2a", "tpf_dp_param_ag_gemm", "tpf_sym_bytes_dp_ag", "tpf_gemm",
-    "tpf_swiglu", "tpf_sym_bytes_ag", "tpf_sym_bytes_rs",
+    "tpf_version",
+    "tpf_last_error",
+    "tpf_device_sms",
+    "tpf_ring_indices",
+    "tpf_schedule_build",
+    "tpf_schedule_check",
+    "tpf_comm_create",
+    "tpf_comm_ipc_handle",
+    "tpf_comm_open_peers",
+    "tpf_comm_create_local_group",
+    "tpf_comm_destroy",
+    "tpf_comm_rank",
+    "tpf_comm_world",
+    "tpf_comm_sync",
+    "tpf_comm_set_timeout_ns",
+    "tpf_comm_inject_fault",
+    "tpf_comm_set_compute_only",
+    "tpf_comm_set_trace",
+    "tpf_ag_gemm",
+    "tpf_gemm_rs",
+    "tpf_dp_grad_rs",
+    "tpf_attention_a2a",
+    "tpf_query_split_attention",
+    "tpf_dp_param_ag_gemm",
+    "tpf_sym_bytes_dp_ag",
+    "tpf_gemm",
+    "tpf_swiglu",
+    "tpf_sym_bytes_ag",
+    "tpf_sym_bytes_rs",
 )
 
 
@@ -294,6 +319,20 @@ def _attention_a2a(self, q, k, v, out, batch: int, heads: int, scale: bool = Tru
 
 
 Communicator.attention_a2a = _attention_a2a
+
+
+def _query_split_attention(self, q, k, v, w_o, out, batch: int, heads: int, kind: int = RING,
+                           wire: int = F32, scale: bool = True, stream=None) -> None:
+    """query_split_attention (Alg. 4, layers.cpp:149-172). Per rank q/k/v: (batch*heads, S, 128)
+    bf16, w_o: (heads*128, D) bf16 (row shard), out: (batch, S/T, D). Local groups: rank-stacked."""
+    S, Dh = q.shape[-2:]
+    D = w_o.shape[-1]
+    _check(_lib.tpf_query_split_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), w_o.data_ptr(),
+                                          out.data_ptr(), batch, heads, S, Dh, D, kind, wire, _dtype_code(out),
+                                          int(bool(scale)), _stream_ptr(stream)))
+
+
+Communicator.query_split_attention = _query_split_attention
 
 
 def sym_bytes_dp_ag(world, K, N_local) -> int:

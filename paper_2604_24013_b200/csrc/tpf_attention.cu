@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256, 1) tpf_fmha_a2a_kernel(const __grid_const
       for (int it = c; it < nitems; it += C, ++ic) {
         const int step = it / per_step, rem = it - step * per_step;
         const int g = rem / p.nqt, qt = rem - g * p.nqt;
-        const int l = (rank + step + 1) % p.T;
+        const int l = p.local ? 0 : (rank + step + 1) % p.T;
         const int row0 = static_cast<int>(static_cast<int64_t>(l) * p.sl + qt * kFTile);
         fmha_wait(p, q_empty, (ic & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, kFQBytes);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, 1) tpf_fmha_a2a_kernel(const __grid_const
     for (int it = c; it < nitems; it += C) {
       const int step = it / per_step, rem = it - step * per_step;
       const int g = rem / p.nqt, qt = rem - g * p.nqt;
-      const int dst = (rank + step + 1) % p.T;
+      const int dst = p.local ? rank : (rank + step + 1) % p.T;
       float m = -INFINITY, lsum = 0.f;
       for (int j = 0; j < p.nkv; ++j, ++sc) {
         fmha_wait(p, s_full + (sc & 1), (sc >> 1) & 1);
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256, 1) tpf_fmha_a2a_kernel(const __grid_const
       const int b = g / p.heads, hh = g - b * p.heads;
       char* orow = p.recv[dst] +
                    ((static_cast<int64_t>(b) * p.sl + qt * kFTile + row) * p.fw +
-                    (static_cast<int64_t>(rank) * p.heads + hh) * kFTile) * 2;
+                    (static_cast<int64_t>(p.local ? 0 : rank) * p.heads + hh) * kFTile) * 2;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint32_t o[32];

@@ -111,6 +111,7 @@ enum TraceKind : int {
 struct FmhaParams {
   CUtensorMap tmap_q, tmap_k, tmap_v;  // (Dh = 128, S, G, hosted ranks), box (64, 128), SW128
   int T, R, rank0, heads, G, nqt, nkv, ctas_per_rank;
+  int local;                           // 1: plain attention into recv[rank] (no all-to-all)
   int64_t S, sl, fw;                   // fw = T * heads * Dh (output row stride, elements)
   float scale_log2;                    // softmax scale * log2(e)
   char* recv[kMaxRanks];               // every rank's receive buffer (peer-mapped)

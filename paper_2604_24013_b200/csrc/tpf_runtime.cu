@@ -781,6 +781,77 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   return TPF_OK;
 }
 
+int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const void* v, const void* w_o,
+                              void* out, int64_t batch, int64_t heads, int64_t S, int64_t Dh, int64_t D, int kind,
+                              int wire_dtype, int out_dtype, int scale, void* stream_v) {
+  // query_split_attention (Alg. 4, layers.cpp:149-172): context = merge_heads(attention(q, k, v))
+  // for every query slice (fused tcgen05 flash attention, local output), then the fused
+  // GEMM-RS over the row-sharded output projection with the schedule's reduction order.
+  tpf::Status s = check_ready(c);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  std::vector<int32_t> sched;
+  s = tpf::build_schedule(kind, T, sched);
+  if (!s.good()) return fail(s);
+  if (batch < 1 || heads < 1 || S < 1 || D < 1)
+    return fail(tpf::Status::invalid("attention inputs need batch >= 1, heads >= 1"));
+  if (T > 1 && S % T)
+    return fail(tpf::Status::invalid("fuse_reduce_scatter: sequence length " + std::to_string(S) +
+                                     " is not divisible by " + std::to_string(T) + " (group size " +
+                                     std::to_string(T) + " x granularity 1)"));
+  if (Dh != 128 || S % 128 || D % 8)
+    return fail(tpf::Status::shape("query_split_attention: needs head_dim 128, seq % 128 == 0, d % 8 == 0"));
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const int R = hosted(c);
+  const int r0 = c->local_group ? 0 : c->rank;
+  const int64_t G = batch * heads, hd = heads * Dh;
+  const size_t ctx_bytes = static_cast<size_t>(R) * batch * S * hd * 2;
+  if (c->scratch_bytes < ctx_bytes) {
+    if (c->scratch) cudaFree(c->scratch);
+    c->scratch = nullptr;
+    c->scratch_bytes = 0;
+    TPF_CUDA_TRY(cudaMalloc(&c->scratch, ctx_bytes));
+    c->scratch_bytes = ctx_bytes;
+  }
+  tpf::FmhaParams fp;
+  std::memset(&fp, 0, sizeof(fp));
+  const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
+                            static_cast<uint64_t>(R)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2),
+                               static_cast<uint64_t>(G * S * Dh * 2)};
+  const uint32_t box[4] = {64, 128, 1, 1};
+  s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
+  if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
+  if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
+  if (!s.good()) return fail(s);
+  fp.T = 1; fp.local = 1; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
+  fp.nqt = static_cast<int>(S / 128); fp.nkv = static_cast<int>(S / 128);
+  fp.S = S; fp.sl = S; fp.fw = hd;
+  fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
+  for (int hh = 0; hh < R; ++hh) fp.recv[r0 + hh] = c->scratch + static_cast<size_t>(hh) * batch * S * hd * 2;
+  fp.err = c->err;
+  fp.timeout_ns = c->timeout_ns;
+  fp.fault_rank = -1;
+  const int sms = tpf::num_sms();
+  fp.ctas_per_rank = std::max(1, sms / R);
+  tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
+  TPF_CUDA_TRY(cudaGetLastError());
+  Call kc{};
+  kc.op = tpf::OP_RS;
+  kc.T = T;
+  kc.m = 1;
+  kc.direct = kind == TPF_PAIRWISE;
+  kc.wire_f32 = wire_dtype == TPF_F32;
+  kc.out_f32 = out_dtype == TPF_F32;
+  kc.n_hosted = R;
+  kc.rank0 = r0;
+  kc.B = batch; kc.Sc = S / T; kc.K = hd; kc.N = D; kc.x_rows = S; kc.out_rows = S / T;
+  kc.x = c->scratch; kc.w = w_o; kc.out = out;
+  kc.sched = T > 1 ? sched.data() : nullptr;
+  s = launch(c, kc, stream);
+  return s.good() ? TPF_OK : fail(s);
+}
+
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,
              int out_dtype, void* stream) {
   if (M < 1 || K < 1 || N < 1) return fail(tpf::Status::shape("tpf_gemm: dimensions must be positive"));

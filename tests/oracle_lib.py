@@ -57,6 +57,7 @@ class Oracle:
         L.or_fuse_rs_identity.argtypes = [C.c_int] * 3 + [_i64] * 3 + [_D, _D]
         L.or_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
         L.or_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
+        L.or_query_split_attention.argtypes = [C.c_int] * 4 + [_i64] * 3 + [C.c_int, _D, _D, _D, _D, _D]
         self.L = L
 
     @staticmethod
@@ -144,6 +145,19 @@ class Oracle:
         return out.reshape(t, batch, s // t, t * heads * dh)
 
 
+    def query_split_attention(self, t, kind, batch, heads, q, k, v, w_o, scale=True):
+        """q/k/v: (T, batch*heads, S, dh); w_o: (T*heads*dh, d) -> (T, batch, S/T, d)."""
+        _, bh, s, dh = q.shape
+        d = w_o.shape[1]
+        out = np.empty(t * batch * (s // t) * d, np.float64)
+        self._chk(self.L.or_query_split_attention(t, kind, batch, heads, s, dh, d, int(scale),
+                                                  np.ascontiguousarray(q).reshape(-1), np.ascontiguousarray(k).reshape(-1),
+                                                  np.ascontiguousarray(v).reshape(-1),
+                                                  np.ascontiguousarray(w_o).reshape(-1), out),
+                  "query_split_attention: invalid arguments")
+        return out.reshape(t, batch, s // t, d)
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_SO)
 
@@ -164,6 +178,7 @@ class Reference:
         L.ref_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
         L.ref_time_ops.argtypes = [C.c_int] + [_i64] * 6 + [C.c_int, _D, _D]
         L.ref_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
+        L.ref_query_split_attention.argtypes = [C.c_int] * 4 + [_i64] * 3 + [C.c_int, _D, _D, _D, _D, _D]
         self.L = L
 
     def _chk(self, rc):
@@ -229,6 +244,16 @@ class Reference:
                                            np.ascontiguousarray(k).reshape(-1), np.ascontiguousarray(v).reshape(-1),
                                            out))
         return out.reshape(t, batch, s // t, t * heads * dh)
+
+    def query_split_attention(self, t, kind, batch, heads, q, k, v, w_o, scale=True):
+        _, bh, s, dh = q.shape
+        d = w_o.shape[1]
+        out = np.empty(t * batch * (s // t) * d, np.float64)
+        self._chk(self.L.ref_query_split_attention(t, kind, batch, heads, s, dh, d, int(scale),
+                                                   np.ascontiguousarray(q).reshape(-1), np.ascontiguousarray(k).reshape(-1),
+                                                   np.ascontiguousarray(v).reshape(-1),
+                                                   np.ascontiguousarray(w_o).reshape(-1), out))
+        return out.reshape(t, batch, s // t, d)
 
     def time_ops(self, t, b, s, k_ag, n_ag, k_rs, n_rs, reps=1):
         """Per-repetition wall seconds of the reference's AG-GEMM and GEMM-RS."""

@@ -566,3 +566,49 @@ def test_attention_a2a_fused_fmha_vs_oracle(T):
         assert np.isfinite(got).all()
         assert rel_deviation(got, want) <= 2e-2
     comm.close()
+
+
+
+# ------------------------------------------- query-split attention
+@pytest.mark.parametrize("T", [1, 2, 4])
+def test_query_split_attention_vs_oracle(T):
+    """Alg. 4: fuse_reduce_scatter of merge_heads(attention(q_slice)) . W_o[r] (layers.cpp:149-172),
+    every schedule; rel_deviation <= 2e-2 (bf16 P / context) vs the fp64 oracle."""
+    batch, heads, S, Dh, D = 1, 2, 256 * T, 128, 256
+    rng = np.random.default_rng(800 + T)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, (T, batch * heads, S, Dh))) for _ in range(3))
+    w_o = bf16_round(rng.uniform(-1, 1, (T * heads * Dh, D)) / 16)
+    dq, dk, dv = (bf16(a).to(DEV) for a in (q, k, v))
+    dw = bf16(w_o.reshape(T, heads * Dh, D)).to(DEV)
+    out = torch.empty((T, batch, S // T, D), device=DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, batch, S, heads * Dh, D, 1) + (1 << 22))
+    for kind in KINDS:
+        if kind == tpf.PAIRWISE and T % 2 and T != 1:
+            continue
+        comm.query_split_attention(dq, dk, dv, dw, out, batch, heads, kind=kind)
+        comm.sync()
+        want = O.query_split_attention(T, kind, batch, heads, q, k, v, w_o)
+        assert rel_deviation(out.double().cpu().numpy(), want) <= 2e-2, kind
+    comm.close()
+
+
+def test_query_split_equals_row_parallel_on_attention_output():
+    """layers_test.cpp:295-313 analogue: the two FuseRS attention embodiments agree -- the
+    query-split result equals row_parallel_forward applied to the attention context."""
+    T, batch, heads, S, Dh, D = 4, 1, 2, 1024, 128, 256
+    g = torch.Generator(device=DEV).manual_seed(11)
+    q, k, v = (torch.randn((T, batch * heads, S, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3))
+    w = (torch.randn((T, heads * Dh, D), device=DEV, generator=g) / 16).to(torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, batch, S, heads * Dh, D, 1) + (1 << 22))
+    out = torch.empty((T, batch, S // T, D), device=DEV)
+    comm.query_split_attention(q, k, v, w, out, batch, heads)
+    # context by SDPA, merged heads (batch, S, heads*Dh) per rank, then the fused GEMM-RS
+    ctx = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float())
+    ctx = ctx.reshape(T, batch, heads, S, Dh).permute(0, 1, 3, 2, 4).reshape(T, batch, S, heads * Dh)
+    ctx = ctx.to(torch.bfloat16).contiguous()
+    out2 = torch.empty_like(out)
+    comm.gemm_rs(ctx, w, out2)
+    comm.sync()
+    comm.close()
+    err = (out - out2).abs().max().item()
+    assert err <= 2e-2 * out2.abs().max().item(), err

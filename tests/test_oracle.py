@@ -178,3 +178,19 @@ def test_attention_a2a_restatement_bitexact(t):
         for scale in (True, False):
             assert np.array_equal(O.attention_a2a(t, b, heads, q, k, v, scale),
                                   R.attention_a2a(t, b, heads, q, k, v, scale))
+
+
+@needs_ref
+@pytest.mark.parametrize("t", [1, 2, 4])
+def test_query_split_attention_restatement_bitexact(t):
+    """Alg. 4 (query_split_attention): restatement == compiled reference, every schedule."""
+    R = Reference()
+    rng = np.random.default_rng(60 + t)
+    b, heads, s, dh, d = 2, 2, 8 * t, 4, 8
+    q, k, v = (rng.uniform(-1, 1, (t, b * heads, s, dh)) for _ in range(3))
+    w_o = rng.uniform(-1, 1, (t * heads * dh, d))
+    for kind in KINDS:
+        if kind == PAIRWISE and t % 2 and t != 1:
+            continue
+        assert np.array_equal(O.query_split_attention(t, kind, b, heads, q, k, v, w_o),
+                              R.query_split_attention(t, kind, b, heads, q, k, v, w_o))
