@@ -329,6 +329,39 @@ inline void row_parallel_forward(RankEndpoint& ep, const DeviceTensor& x, const 
                             static_cast<int>(schedule.kind), m, wire, out.dtype, stream));
 }
 
+// UP: fuse_all_to_all_attention (layers.hpp:100-101). q/k/v bf16 (batch*heads, S, Dh) for this
+// rank's head group; out bf16 (batch, S/T, T*heads*Dh). Dh == 128 runs the fused tcgen05
+// flash-attention kernel; other head dims run the GEMM-family pipeline.
+inline void fuse_all_to_all_attention(RankEndpoint& ep, const void* q, const void* k, const void* v, void* out,
+                                      int64_t batch, int64_t heads, int64_t S, int64_t Dh, bool scale_scores = true,
+                                      cudaStream_t stream = nullptr) {
+  detail::check(tpf_attention_a2a(ep.handle(), q, k, v, out, batch, heads, S, Dh, scale_scores ? 1 : 0, stream));
+}
+
+// query_split_attention (layers.hpp:88-91): w_o is this rank's (heads*128, D) row shard.
+inline void query_split_attention(RankEndpoint& ep, const void* q, const void* k, const void* v, const void* w_o,
+                                  DeviceTensor& out, int64_t batch, int64_t heads, int64_t S,
+                                  const Schedule& schedule, int wire = TPF_F32, bool scale_scores = true,
+                                  cudaStream_t stream = nullptr) {
+  detail::check(tpf_query_split_attention(ep.handle(), q, k, v, w_o, out.data, batch, heads, S, 128, out.feat,
+                                          static_cast<int>(schedule.kind), wire, out.dtype, scale_scores ? 1 : 0,
+                                          stream));
+}
+
+// DP gradient sync (cfg 4): dW rows [r*K/T, (r+1)*K/T) of sum_q X_q^T dY_q.
+inline void dp_grad_reduce_scatter(RankEndpoint& ep, const void* X, const void* dY, DeviceTensor& dW,
+                                   int64_t M_local, int64_t K, const Schedule& schedule, int m = 1,
+                                   int wire = TPF_F32, cudaStream_t stream = nullptr) {
+  detail::check(tpf_dp_grad_rs(ep.handle(), X, dY, dW.data, M_local, K, dW.feat, static_cast<int>(schedule.kind), m,
+                               wire, dW.dtype, stream));
+}
+
+// DP parameter all-gather fused into the forward GEMM (cfg 4): out = x . W^T, W row-sharded.
+inline void dp_param_all_gather_gemm(RankEndpoint& ep, const void* x, const void* w_rows, DeviceTensor& out,
+                                     int64_t M_local, int64_t K, int64_t N_local, cudaStream_t stream = nullptr) {
+  detail::check(tpf_dp_param_ag_gemm(ep.handle(), x, w_rows, out.data, M_local, K, N_local, out.dtype, stream));
+}
+
 // ------------------------------------------ single-GPU group (spawn_group analogue)
 class LocalGroup {
  public:
