@@ -184,6 +184,20 @@ int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local);
 int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                       int64_t heads, int64_t S, int64_t Dh, int scale, void* stream);
 
+// Ulysses first all-to-all (the ref_all_to_all step of
+// layers_test.cpp:347-397, fabric.cpp:183-207): per rank q/k/v (batch*heads_total, S/T, Dh)
+// bf16, sequence-sharded with every head -> q_out/k_out/v_out (batch*heads_total/T, S, Dh),
+// this rank's head group over the whole sequence. Peer stores over NVLink + flags.
+int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* q_out, void* k_out, void* v_out,
+                    int64_t batch, int64_t heads_total, int64_t S, int64_t Dh, void* stream);
+
+// Whole UP layer (Ulysses attention, paper Alg. 5 with its first all-to-all): the first
+// all-to-all above into the symmetric inbox, then fuse_all_to_all_attention (layers.cpp:174-218)
+// reading straight from the inbox. q/k/v as tpf_ulysses_a2a; out (batch, S/T, heads_total*Dh)
+// bf16. Needs Dh == 128 and (S/T) % 128 == 0.
+int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
+                          int64_t heads_total, int64_t S, int64_t Dh, int scale, void* stream);
+
 /* Query-split attention (Alg. 4). Replaces:
  *   Tensor query_split_attention(RankEndpoint&, const AttentionInputs&, const ShardedLinear& out_proj,
  *                                const Schedule&, const AttentionOptions&)  (layers.hpp:88-91,

@@ -14,11 +14,13 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "tpfuse/collectives.hpp"
+#include "tpfuse/experiment.hpp"
 #include "tpfuse/fabric.hpp"
 #include "tpfuse/layers.hpp"
 #include "tpfuse/tensor.hpp"
@@ -278,6 +280,59 @@ extern "C" int ref_query_split_attention(int t, int kind, int batch, int heads, 
     opt.scale_scores = scale != 0;
     auto outs = tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
       return tpfuse::query_split_attention(ep, in[ep.rank()], wo, sched, opt);
+    });
+    size_t off = 0;
+    for (auto& o : outs) {
+      copy_out(o, out + off);
+      off += o.raw().size();
+    }
+  });
+}
+
+// Bench CSV wire format (experiment.cpp:838-860): runs the reference's own run_bench on a
+// small config and returns its CSV text, so the GPU bench's rows can be checked field by
+// field against the reference's formatting.
+extern "C" int ref_bench_csv(const char* layer, int tp, int64_t batch, int64_t seq, int64_t d_model, int heads,
+                             int granularity, const char* schedule, uint64_t seed, int reps, char* buf,
+                             int64_t cap) {
+  return guarded([&] {
+    tpfuse::ExperimentConfig cfg;
+    cfg.layer = tpfuse::layer_kind_from_string(layer);
+    cfg.schedule = tpfuse::schedule_kind_from_string(schedule);
+    cfg.tp_size = tp;
+    cfg.batch = batch;
+    cfg.seq = seq;
+    cfg.d_model = d_model;
+    cfg.heads = heads;
+    cfg.granularity = granularity;
+    cfg.seed = seed;
+    cfg.reps = reps;
+    std::ostringstream csv;
+    tpfuse::run_bench(cfg, csv);
+    const std::string s = csv.str();
+    if (static_cast<int64_t>(s.size()) + 1 > cap) throw std::length_error("ref_bench_csv: buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+// Ulysses first all-to-all exactly as layers_test.cpp:347-397 drives it: per-group parts of
+// this rank's sequence slice, tpfuse::ref_all_to_all, tpfuse::concat_seq.
+extern "C" int ref_ulysses_a2a(int t, int batch, int heads, int64_t s, int64_t dh, const double* in, double* out) {
+  return guarded([&] {
+    const int64_t sl = s / t, hl = heads / t, bh = static_cast<int64_t>(batch) * heads;
+    auto outs = tpfuse::spawn_group(t, [&](tpfuse::RankEndpoint& ep) {
+      const int r = ep.rank();
+      const tpfuse::Tensor slice = tensor_from(in + r * bh * sl * dh, bh, sl, dh);
+      std::vector<tpfuse::Tensor> parts;
+      for (int g = 0; g < t; ++g) {
+        tpfuse::Tensor p(static_cast<int64_t>(batch) * hl, sl, dh);
+        for (int64_t b = 0; b < batch; ++b)
+          for (int64_t h = 0; h < hl; ++h)
+            for (int64_t i = 0; i < sl; ++i)
+              for (int64_t d = 0; d < dh; ++d) p(b * hl + h, i, d) = slice(b * heads + g * hl + h, i, d);
+        parts.push_back(std::move(p));
+      }
+      return tpfuse::concat_seq(tpfuse::ref_all_to_all(ep, parts));
     });
     size_t off = 0;
     for (auto& o : outs) {

@@ -513,3 +513,24 @@ int or_query_split_attention(int t, int kind, int batch, int heads, int64_t s, i
   free(sched); free(parts); free(scores); free(o); free(ctx);
   return rc;
 }
+
+/* Ulysses first all-to-all. Restates layers_test.cpp:347-397's
+ * to_head_sharded: rank r splits its sequence slice (batch*heads, S/T, dh) into T head-group
+ * parts p_g(b*hl + h, s, d) = slice(b*heads + g*hl + h, s, d) (hl = heads/T), trades them with
+ * ref_all_to_all (fabric.cpp:183-207: out[k] on rank r = parts[r] of rank k), then concat_seq
+ * (tensor.cpp) stacks the received parts in source-rank order along the sequence.
+ * in: T stacked (batch*heads, S/T, dh); out: T stacked (batch*hl, S, dh). */
+int or_ulysses_a2a(int t, int batch, int heads, int64_t s, int64_t dh, const double* in, double* out) {
+  if (t < 1 || batch < 1 || heads < 1 || s % t != 0 || heads % t != 0) return -1;
+  const int64_t sl = s / t, hl = heads / t;
+  const int64_t in_per = (int64_t)batch * heads * sl * dh, out_per = (int64_t)batch * hl * s * dh;
+  for (int g = 0; g < t; ++g)            /* receiving rank = head group */
+    for (int src = 0; src < t; ++src)    /* sending rank = sequence slice */
+      for (int64_t b = 0; b < batch; ++b)
+        for (int64_t h = 0; h < hl; ++h)
+          for (int64_t i = 0; i < sl; ++i)
+            for (int64_t d = 0; d < dh; ++d)
+              out[g * out_per + ((b * hl + h) * s + src * sl + i) * dh + d] =
+                  in[src * in_per + ((b * heads + g * hl + h) * sl + i) * dh + d];
+  return 0;
+}

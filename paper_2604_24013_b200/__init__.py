@@ -76,6 +76,8 @@ _lib.tpf_dp_grad_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int] * 4
 _lib.tpf_dp_param_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
 _lib.tpf_attention_a2a.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
 _lib.tpf_query_split_attention.argtypes = [_vp] * 6 + [_i64] * 5 + [C.c_int] * 4 + [_vp]
+_lib.tpf_ulysses_a2a.argtypes = [_vp] * 7 + [_i64] * 4 + [_vp]
+_lib.tpf_ulysses_attention.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
 _lib.tpf_sym_bytes_dp_ag.argtypes = [C.c_int, _i64, _i64]
 _lib.tpf_sym_bytes_dp_ag.restype = _i64
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
@@ -108,6 +110,8 @@ EXPORTED_SYMBOLS = (
     "tpf_dp_grad_rs",
     "tpf_attention_a2a",
     "tpf_query_split_attention",
+    "tpf_ulysses_a2a",
+    "tpf_ulysses_attention",
     "tpf_dp_param_ag_gemm",
     "tpf_sym_bytes_dp_ag",
     "tpf_gemm",
@@ -333,6 +337,39 @@ def _query_split_attention(self, q, k, v, w_o, out, batch: int, heads: int, kind
 
 
 Communicator.query_split_attention = _query_split_attention
+
+
+def _ulysses_a2a(self, q, k, v, q_out, k_out, v_out, batch: int, heads: int, stream=None) -> None:
+    """Ulysses first all-to-all (ref_all_to_all of layers_test.cpp:347-397):
+    per rank q/k/v (batch*heads, S/T, Dh) bf16 with every head -> (batch*heads/T, S, Dh), this
+    rank's head group over the whole sequence. Local groups: rank-stacked."""
+    sl, Dh = q.shape[-2:]
+    _check(_lib.tpf_ulysses_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), q_out.data_ptr(),
+                                k_out.data_ptr(), v_out.data_ptr(), batch, heads, sl * self.world, Dh,
+                                _stream_ptr(stream)))
+
+
+Communicator.ulysses_a2a = _ulysses_a2a
+
+
+def _ulysses_attention(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
+    """The whole UP attention (Alg. 5 with its first all-to-all): sequence-sharded q/k/v
+    (batch*heads, S/T, 128) per rank -> out (batch, S/T, heads*128), with both all-to-alls fused
+    (peer-store inbox + fused flash attention pushing O tiles to the slice owner)."""
+    sl, Dh = q.shape[-2:]
+    _check(_lib.tpf_ulysses_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch,
+                                      heads, sl * self.world, Dh, int(bool(scale)), _stream_ptr(stream)))
+
+
+Communicator.ulysses_attention = _ulysses_attention
+
+
+def sym_bytes_ulysses(world, batch, heads, S, Dh=128) -> int:
+    """Symmetric heap bytes per rank for ulysses_attention (and ulysses_a2a)."""
+    sl, hl = S // world, heads // world
+    out_area = batch * sl * heads * Dh * 2
+    inbox = 3 * batch * hl * S * Dh * 2
+    return 2 * (((out_area + 4095) // 4096) * 4096 + inbox) + 2 * (1 << 20) + 8192
 
 
 def sym_bytes_dp_ag(world, K, N_local) -> int:

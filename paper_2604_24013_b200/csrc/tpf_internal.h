@@ -123,6 +123,20 @@ struct FmhaParams {
   int64_t timeout_ns;
 };
 
+// Ulysses first all-to-all (tpf_ulysses.cu): sequence-sharded Q/K/V -> head-sharded.
+struct UlyssesParams {
+  const char* src[3];               // q, k, v of hosted rank 0: (B*H, sl, Dh) bf16
+  int64_t src_rank_stride;          // bytes between hosted ranks' inputs
+  char* dst[kMaxRanks];             // every rank's inbox: [q | k | v], each (B*hl, S, Dh)
+  uint32_t* flags[kMaxRanks];       // every rank's a2a flag block: [src rank][cta]
+  int64_t tensor_bytes;             // B*hl*S*Dh*2
+  int64_t B, H, hl, S, sl, Dh;
+  int T, R, rank0, ctas_per_rank;
+  uint32_t epoch;
+  int fault_rank;
+};
+
+void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream);
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
 void launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);

@@ -33,6 +33,13 @@ int fail(const tpf::Status& s) {
       return fail(tpf::Status::cuda(std::string(#expr) + ": " + cudaGetErrorString(e_))); \
   } while (0)
 
+#define TPF_CUDA_TRY_STATUS(expr)                                                   \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return tpf::Status::cuda(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
 constexpr int64_t kFlagBytesPerParity = 1 << 20;  // 256 Ki flags per parity
 constexpr int64_t kDefaultTimeoutNs = 10ll * 1000 * 1000 * 1000;
 
@@ -645,6 +652,64 @@ int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* o
   return s.good() ? TPF_OK : fail(s);
 }
 
+// Fused flash attention + output all-to-all (UP v2, Dh = 128). q/k/v: (G, S, 128) bf16 per hosted
+// rank, hosted ranks `rstride` bytes apart. Uses (and does not bump) `epoch`.
+static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* q, const void* k, const void* v, uint64_t rstride,
+                               void* out, int64_t batch, int64_t heads, int64_t S, uint32_t epoch, int scale,
+                               cudaStream_t stream) {
+  const int T = c->world;
+  const int R = hosted(c);
+  const int r0 = c->local_group ? 0 : c->rank;
+  const int64_t Dh = 128, G = batch * heads, sl = S / T, fw = static_cast<int64_t>(T) * heads * Dh;
+  const int64_t recv_bytes = batch * sl * fw * 2;
+  const int64_t nflags2 = G * (sl / 128) * 4;
+  if (nflags2 * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
+    return tpf::Status::capacity("symmetric heap too small for the attention all-to-all");
+  const int par = static_cast<int>(epoch & 1u);
+  auto recv_at = [&](int rank) {
+    return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes);
+  };
+  auto flags_at = [&](int rank) { return reinterpret_cast<uint32_t*>(c->sym[rank] + par * kFlagBytesPerParity); };
+  tpf::FmhaParams fp;
+  std::memset(&fp, 0, sizeof(fp));
+  const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
+                            static_cast<uint64_t>(R)};
+  const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2), rstride};
+  const uint32_t box[4] = {64, 128, 1, 1};
+  tpf::Status s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
+  if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
+  if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
+  if (!s.good()) return s;
+  fp.T = T; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
+  fp.nqt = static_cast<int>(sl / 128); fp.nkv = static_cast<int>(S / 128);
+  fp.S = S; fp.sl = sl; fp.fw = fw;
+  fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
+  for (int x = 0; x < T; ++x) {
+    fp.recv[x] = recv_at(x);
+    fp.flags[x] = flags_at(x);
+  }
+  fp.nflags_per_src = nflags2;
+  fp.epoch = epoch;
+  fp.fault_rank = c->fault_rank;
+  fp.err = c->err;
+  fp.timeout_ns = c->timeout_ns;
+  const int sms = tpf::num_sms();
+  fp.ctas_per_rank = std::max(1, sms / R);
+  tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
+  TPF_CUDA_TRY_STATUS(cudaGetLastError());
+  for (int hh = 0; hh < R; ++hh) {
+    const int rank = r0 + hh;
+    uint32_t* f = flags_at(rank);
+    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags2, epoch, c->timeout_ns, c->err, rank, stream);
+    tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags2, static_cast<int64_t>(T - 1 - rank) * nflags2,
+                           epoch, c->timeout_ns, c->err, rank, stream);
+    TPF_CUDA_TRY_STATUS(cudaMemcpyAsync(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank), recv_bytes,
+                                        cudaMemcpyDeviceToDevice, stream));
+  }
+  TPF_CUDA_TRY_STATUS(cudaGetLastError());
+  return tpf::Status::ok();
+}
+
 int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                       int64_t heads, int64_t S, int64_t Dh, int scale, void* stream_v) {
   // fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218) on the GEMM kernel family.
@@ -674,51 +739,10 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   };
   if (Dh == 128 && sl % 128 == 0) {
     // v2: one persistent fused flash-attention launch for all steps / heads / hosted ranks
-    tpf::FmhaParams fp;
-    std::memset(&fp, 0, sizeof(fp));
-    const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
-                              static_cast<uint64_t>(R)};
-    const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2),
-                                 static_cast<uint64_t>(G * S * Dh * 2)};
-    const uint32_t box[4] = {64, 128, 1, 1};
-    s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
-    if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
-    if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
-    if (!s.good()) return fail(s);
-    const int64_t nflags2 = G * (sl / 128) * 4;
-    if (nflags2 * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
-      return fail(tpf::Status::capacity("symmetric heap too small for the attention all-to-all"));
     c->epoch += 1;
-    const uint32_t epoch = c->epoch;
-    const int par = static_cast<int>(epoch & 1u);
-    fp.T = T; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
-    fp.nqt = static_cast<int>(sl / 128); fp.nkv = static_cast<int>(S / 128);
-    fp.S = S; fp.sl = sl; fp.fw = fw;
-    fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
-    for (int x = 0; x < T; ++x) {
-      fp.recv[x] = recv_at(x, par);
-      fp.flags[x] = flags_at(x, par);
-    }
-    fp.nflags_per_src = nflags2;
-    fp.epoch = epoch;
-    fp.fault_rank = c->fault_rank;
-    fp.err = c->err;
-    fp.timeout_ns = c->timeout_ns;
-    const int sms = tpf::num_sms();
-    fp.ctas_per_rank = std::max(1, sms / R);
-    tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
-    TPF_CUDA_TRY(cudaGetLastError());
-    for (int hh = 0; hh < R; ++hh) {
-      const int rank = r0 + hh;
-      uint32_t* f = flags_at(rank, par);
-      tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags2, epoch, c->timeout_ns, c->err, rank, stream);
-      tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags2, static_cast<int64_t>(T - 1 - rank) * nflags2,
-                             epoch, c->timeout_ns, c->err, rank, stream);
-      TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank, par), recv_bytes,
-                                   cudaMemcpyDeviceToDevice, stream));
-    }
-    TPF_CUDA_TRY(cudaGetLastError());
-    return TPF_OK;
+    s = fmha_a2a_v2(c, q, k, v, static_cast<uint64_t>(G * S * Dh * 2), out, batch, heads, S, c->epoch, scale,
+                    stream);
+    return s.good() ? TPF_OK : fail(s);
   }
   // v1 (any head_dim): scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S)
   const size_t sc_bytes = static_cast<size_t>(R) * G * sl * S * 4, pb_bytes = sc_bytes / 2;
@@ -952,3 +976,110 @@ int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- Ulysses (UP end to end)
+// First all-to-all (sequence-sharded -> head-sharded Q/K/V, peer stores into every rank's
+// symmetric inbox), then the fused flash attention whose epilogue performs the second
+// all-to-all (fuse_all_to_all_attention). Inbox layout per parity, after the attention's
+// output area: [q | k | v], each (batch*heads_local, S, Dh) bf16. The a2a flags sit after
+// the attention's flags in the same parity block: [source rank][cta].
+static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, const void* v, int64_t batch,
+                                     int64_t heads_total, int64_t S, int64_t Dh, uint32_t epoch,
+                                     int64_t out_area_bytes, int64_t flag_off, char** inbox_local,
+                                     cudaStream_t stream) {
+  const int T = c->world;
+  const int R = hosted(c);
+  const int r0 = c->local_group ? 0 : c->rank;
+  const int64_t hl = heads_total / T, sl = S / T;
+  const int64_t tensor_bytes = batch * hl * S * Dh * 2;
+  const int par = static_cast<int>(epoch & 1u);
+  const int64_t inbox_off = (out_area_bytes + 4095) & ~int64_t{4095};
+  if (inbox_off + 3 * tensor_bytes > data_bytes_per_parity(c->sym_bytes))
+    return tpf::Status::capacity("symmetric heap too small for the Ulysses all-to-all (need " +
+                                 std::to_string(2 * (inbox_off + 3 * tensor_bytes) + 2 * kFlagBytesPerParity) +
+                                 " bytes per rank)");
+  tpf::UlyssesParams up;
+  std::memset(&up, 0, sizeof(up));
+  up.src[0] = static_cast<const char*>(q);
+  up.src[1] = static_cast<const char*>(k);
+  up.src[2] = static_cast<const char*>(v);
+  up.src_rank_stride = batch * heads_total * sl * Dh * 2;
+  up.tensor_bytes = tensor_bytes;
+  up.B = batch; up.H = heads_total; up.hl = hl; up.S = S; up.sl = sl; up.Dh = Dh;
+  up.T = T; up.R = R; up.rank0 = r0;
+  up.ctas_per_rank = std::max(1, std::min(tpf::num_sms() / R, 132));
+  if ((flag_off + static_cast<int64_t>(T) * up.ctas_per_rank) * 4 > kFlagBytesPerParity)
+    return tpf::Status::capacity("flag block too small for the Ulysses all-to-all");
+  for (int x = 0; x < T; ++x) {
+    up.dst[x] = c->sym[x] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes) + inbox_off;
+    up.flags[x] = reinterpret_cast<uint32_t*>(c->sym[x] + par * kFlagBytesPerParity) + flag_off;
+  }
+  up.epoch = epoch;
+  up.fault_rank = c->fault_rank;
+  tpf::launch_ulysses_push(up, stream);
+  TPF_CUDA_TRY_STATUS(cudaGetLastError());
+  for (int hh = 0; hh < R; ++hh) {
+    const int rank = r0 + hh;
+    tpf::launch_wait_flags(up.flags[rank], static_cast<int64_t>(T) * up.ctas_per_rank, epoch, c->timeout_ns, c->err,
+                           rank, stream);
+  }
+  *inbox_local = up.dst[r0];
+  return tpf::Status::ok();
+}
+
+static tpf::Status check_ulysses(tpf_comm* c, int64_t batch, int64_t heads_total, int64_t S, int64_t Dh) {
+  const int T = c->world;
+  if (batch < 1 || heads_total < 1 || S < 1 || Dh < 1)
+    return tpf::Status::invalid("Ulysses inputs need batch >= 1, heads >= 1, seq >= 1, head_dim >= 1");
+  if (S % T)
+    return tpf::Status::invalid("Ulysses: sequence length " + std::to_string(S) +
+                                " is not divisible by group size " + std::to_string(T));
+  if (heads_total % T)
+    return tpf::Status::invalid("Ulysses: head count " + std::to_string(heads_total) +
+                                " is not divisible by group size " + std::to_string(T));
+  if (Dh % 8) return tpf::Status::shape("Ulysses: head_dim must be a multiple of 8");
+  return tpf::Status::ok();
+}
+
+int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* q_out, void* k_out, void* v_out,
+                    int64_t batch, int64_t heads_total, int64_t S, int64_t Dh, void* stream_v) {
+  tpf::Status s = check_ready(c);
+  if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
+  if (!s.good()) return fail(s);
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  c->epoch += 1;
+  char* inbox = nullptr;
+  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, c->epoch, 0, 0, &inbox, stream);
+  if (!s.good()) return fail(s);
+  const int64_t tb = batch * (heads_total / c->world) * S * Dh * 2;
+  void* outs[3] = {q_out, k_out, v_out};
+  for (int hh = 0; hh < hosted(c); ++hh)
+    for (int t = 0; t < 3; ++t)
+      TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(outs[t]) + hh * tb, inbox + hh * c->sym_bytes + t * tb, tb,
+                                   cudaMemcpyDeviceToDevice, stream));
+  return TPF_OK;
+}
+
+int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
+                          int64_t heads_total, int64_t S, int64_t Dh, int scale, void* stream_v) {
+  tpf::Status s = check_ready(c);
+  if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
+  if (!s.good()) return fail(s);
+  const int T = c->world;
+  const int64_t hl = heads_total / T, sl = S / T;
+  if (Dh != 128 || sl % 128)
+    return fail(tpf::Status::shape("tpf_ulysses_attention: the fused path needs head_dim 128 and S/T % 128 == 0"));
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  c->epoch += 1;
+  const uint32_t epoch = c->epoch;
+  const int64_t out_area = batch * sl * heads_total * Dh * 2;
+  const int64_t attn_flags = batch * hl * (sl / 128) * 4 * T;
+  char* inbox = nullptr;
+  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, epoch, out_area, (attn_flags + 31) & ~int64_t{31},
+                        &inbox, stream);
+  if (!s.good()) return fail(s);
+  const int64_t tb = batch * hl * S * Dh * 2;
+  s = fmha_a2a_v2(c, inbox, inbox + tb, inbox + 2 * tb, static_cast<uint64_t>(c->sym_bytes), out, batch, hl, S, epoch,
+                  scale, stream);
+  return s.good() ? TPF_OK : fail(s);
+}

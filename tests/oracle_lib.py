@@ -58,6 +58,7 @@ class Oracle:
         L.or_mlp_square.argtypes = [C.c_int] * 3 + [_i64] * 4 + [_D, _D, _D, _D]
         L.or_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
         L.or_query_split_attention.argtypes = [C.c_int] * 4 + [_i64] * 3 + [C.c_int, _D, _D, _D, _D, _D]
+        L.or_ulysses_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [_D, _D]
         self.L = L
 
     @staticmethod
@@ -158,6 +159,14 @@ class Oracle:
         return out.reshape(t, batch, s // t, d)
 
 
+    def ulysses_a2a(self, t, batch, heads, x):
+        """x: (T, batch*heads, S/T, dh) sequence-sharded -> (T, batch*heads/T, S, dh) head-sharded."""
+        _, bh, sl, dh = x.shape
+        out = np.empty(x.size, np.float64)
+        self._chk(self.L.or_ulysses_a2a(t, batch, heads, sl * t, dh, np.ascontiguousarray(x, np.float64).reshape(-1), out), "ulysses_a2a: invalid arguments")
+        return out.reshape(t, batch * heads // t, sl * t, dh)
+
+
 def have_reference() -> bool:
     return os.path.exists(REF_SO)
 
@@ -179,6 +188,7 @@ class Reference:
         L.ref_time_ops.argtypes = [C.c_int] + [_i64] * 6 + [C.c_int, _D, _D]
         L.ref_attention_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [C.c_int, _D, _D, _D, _D]
         L.ref_query_split_attention.argtypes = [C.c_int] * 4 + [_i64] * 3 + [C.c_int, _D, _D, _D, _D, _D]
+        L.ref_ulysses_a2a.argtypes = [C.c_int] * 3 + [_i64] * 2 + [_D, _D]
         self.L = L
 
     def _chk(self, rc):
@@ -255,9 +265,26 @@ class Reference:
                                                    np.ascontiguousarray(w_o).reshape(-1), out))
         return out.reshape(t, batch, s // t, d)
 
+    def ulysses_a2a(self, t, batch, heads, x):
+        """x: (T, batch*heads, S/T, dh) sequence-sharded -> (T, batch*heads/T, S, dh) head-sharded."""
+        _, bh, sl, dh = x.shape
+        out = np.empty(x.size, np.float64)
+        self._chk(self.L.ref_ulysses_a2a(t, batch, heads, sl * t, dh, np.ascontiguousarray(x, np.float64).reshape(-1), out))
+        return out.reshape(t, batch * heads // t, sl * t, dh)
+
     def time_ops(self, t, b, s, k_ag, n_ag, k_rs, n_rs, reps=1):
         """Per-repetition wall seconds of the reference's AG-GEMM and GEMM-RS."""
         ag = np.zeros(reps, np.float64)
         rs = np.zeros(reps, np.float64)
         self._chk(self.L.ref_time_ops(t, b, s, k_ag, n_ag, k_rs, n_rs, reps, ag, rs))
         return ag.tolist(), rs.tolist()
+
+    def bench_csv(self, layer="mlp", tp=4, batch=2, seq=64, d_model=32, heads=4, granularity=1,
+                  schedule="ring", seed=0, reps=2) -> str:
+        """The reference's own run_bench CSV text (experiment.cpp:842-860) for a small config."""
+        buf = C.create_string_buffer(1 << 16)
+        self.L.ref_bench_csv.argtypes = [C.c_char_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                         C.c_char_p, C.c_uint64, C.c_int, C.c_char_p, C.c_int64]
+        self._chk(self.L.ref_bench_csv(layer.encode(), tp, batch, seq, d_model, heads, granularity,
+                                       schedule.encode(), seed, reps, buf, len(buf)))
+        return buf.value.decode()

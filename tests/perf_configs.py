@@ -111,6 +111,22 @@ def main():
     C["cfg5_up_T8_S32768"] = {"ms": round(t, 3), "tflops": round(flops / (t * 1e-3) / 1e12, 1),
                               "note": "v2: one persistent tcgen05 flash-attention launch (S, O in TMEM, P in SMEM) "
                                       "whose epilogue pushes O tiles to the slice owner + flags"}
+    # cfg5 end to end: sequence-sharded q/k/v -> first all-to-all -> fused attention -> output a2a
+    H = T * heads
+    qs, ks, vs = (rnd((T, H, S // T, Dh), 1.0, 20 + i) for i in range(3))
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, 1, H, S, Dh))
+    t_full = timeit(lambda: comm.ulysses_attention(qs, ks, vs, o, 1, H), n=1, warm=1, reps=2)
+    hq, hk, hv = (torch.empty((T, heads, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3))
+    t_a2a = timeit(lambda: comm.ulysses_a2a(qs, ks, vs, hq, hk, hv, 1, H), n=3, warm=1, reps=3)
+    comm.sync()
+    comm.close()
+    a2a_bytes = 3 * T * H * (S // T) * Dh * 2  # every element read once and written once
+    C["cfg5_up_T8_S32768_end_to_end"] = {
+        "ms": round(t_full, 3), "tflops": round(flops / (t_full * 1e-3) / 1e12, 1),
+        "first_a2a_standalone_ms": round(t_a2a, 3),
+        "first_a2a_GBps_per_direction": round(a2a_bytes / (t_a2a * 1e-3) / 1e9, 1),
+        "note": "ulysses_attention: first all-to-all (peer stores into the symmetric inbox) + the fused "
+                "attention reading the inbox; standalone a2a time includes the inbox -> user copy"}
     os.makedirs(os.path.dirname(out_path) or ".", exist_ok=True)
     with open(out_path, "w") as f:
         json.dump(res, f, indent=1)

@@ -612,3 +612,65 @@ def test_query_split_equals_row_parallel_on_attention_output():
     comm.close()
     err = (out - out2).abs().max().item()
     assert err <= 2e-2 * out2.abs().max().item(), err
+
+
+@pytest.mark.parametrize("T", [1, 2, 4, 8])
+def test_ulysses_first_a2a_bitexact(T):
+    """Ulysses first all-to-all: pure data movement over peer stores,
+    bit-exact against the oracle restatement (pinned to ref_all_to_all)."""
+    batch, heads, sl, Dh = 2, 2 * T, 192, 128
+    rng = np.random.default_rng(900 + T)
+    xs = [bf16_round(rng.uniform(-1, 1, (T, batch * heads, sl, Dh))) for _ in range(3)]
+    dq, dk, dv = (bf16(a).to(DEV) for a in xs)
+    outs = [torch.full((T, batch * heads // T, sl * T, Dh), float("nan"), device=DEV, dtype=torch.bfloat16)
+            for _ in range(3)]
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, heads, sl * T, Dh))
+    for _ in range(3):  # both heap parities, then the first again
+        comm.ulysses_a2a(dq, dk, dv, *outs, batch, heads)
+        comm.sync()
+        for x, o in zip(xs, outs):
+            assert np.array_equal(o.double().cpu().numpy(), O.ulysses_a2a(T, batch, heads, x))
+    comm.close()
+
+
+@pytest.mark.parametrize("T", [1, 2, 4])
+def test_ulysses_attention_end_to_end(T):
+    """The whole UP layer from the sequence-sharded layout (layers_test.cpp:347-397
+    FullFlowFromSequenceShardedLayout): first all-to-all + fused attention + output all-to-all.
+    Within 2e-2 of the fp64 oracle chain, and identical to ulysses_a2a followed by attention_a2a."""
+    batch, heads, sl, Dh = 1, 2 * T, 256, 128
+    S = sl * T
+    rng = np.random.default_rng(950 + T)
+    xs = [bf16_round(rng.uniform(-1, 1, (T, batch * heads, sl, Dh))) for _ in range(3)]
+    hs = [O.ulysses_a2a(T, batch, heads, x) for x in xs]
+    want = O.attention_a2a(T, batch, heads // T, *hs, True)
+    dq, dk, dv = (bf16(a).to(DEV) for a in xs)
+    out = torch.full((T, batch, sl, heads * Dh), float("nan"), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, heads, S, Dh))
+    for _ in range(3):
+        comm.ulysses_attention(dq, dk, dv, out, batch, heads)
+        comm.sync()
+        got = out.double().cpu().numpy()
+        assert np.isfinite(got).all()
+        assert rel_deviation(got, want) <= 2e-2
+    hq, hk, hv = (torch.empty((T, batch * heads // T, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3))
+    comm.ulysses_a2a(dq, dk, dv, hq, hk, hv, batch, heads)
+    out2 = torch.empty_like(out)
+    comm.attention_a2a(hq, hk, hv, out2, batch, heads // T)
+    comm.sync()
+    comm.close()
+    assert torch.equal(out, out2)
+
+
+def test_ulysses_rejects_bad_shapes():
+    comm = tpf.Communicator.local_group(2, 1 << 24)
+    q = torch.zeros((2, 3, 128, 128), device=DEV, dtype=torch.bfloat16)
+    with pytest.raises(ValueError):  # 3 heads over 2 ranks
+        comm.ulysses_a2a(q, q, q, q, q, q, 1, 3)
+    small = tpf.Communicator.local_group(2, 1 << 22)
+    q = torch.zeros((2, 4, 1024, 128), device=DEV, dtype=torch.bfloat16)
+    o = torch.zeros((2, 1, 1024, 512), device=DEV, dtype=torch.bfloat16)
+    with pytest.raises(tpf.CapacityError):
+        small.ulysses_attention(q, q, q, o, 1, 4)
+    comm.close()
+    small.close()

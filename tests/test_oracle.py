@@ -194,3 +194,25 @@ def test_query_split_attention_restatement_bitexact(t):
             continue
         assert np.array_equal(O.query_split_attention(t, kind, b, heads, q, k, v, w_o),
                               R.query_split_attention(t, kind, b, heads, q, k, v, w_o))
+
+
+@needs_ref
+@pytest.mark.parametrize("t", [1, 2, 4])
+def test_ulysses_a2a_restatement_bitexact(t):
+    """Ulysses first all-to-all (layers_test.cpp:347-397 drive of ref_all_to_all): restatement
+    == compiled reference, and it reproduces the direct head-group layout."""
+    R = Reference()
+    rng = np.random.default_rng(90 + t)
+    b, heads, sl, dh = 2, 2 * t, 3, 4
+    x = rng.uniform(-1, 1, (t, b * heads, sl, dh))
+    got = O.ulysses_a2a(t, b, heads, x)
+    assert np.array_equal(got, R.ulysses_a2a(t, b, heads, x))
+    full = x.reshape(t, b, heads, sl, dh).transpose(1, 2, 0, 3, 4).reshape(b, heads, t * sl, dh)
+    hl = heads // t
+    for g in range(t):
+        assert np.array_equal(got[g], full[:, g * hl:(g + 1) * hl].reshape(b * hl, t * sl, dh))
+
+
+def test_ulysses_a2a_rejects_indivisible():
+    with pytest.raises(OracleError):
+        O.ulysses_a2a(3, 1, 4, np.zeros((3, 4, 2, 4)))
