@@ -63,12 +63,12 @@ class BenchConfig:
             raise ValueError("tp_size must be >= 1")
         if self.batch < 1 or self.seq < 1 or self.d_model < 1 or self.heads < 1:
             raise ValueError("batch, seq, d_model and heads must be >= 1")
-        if self.seq % t:
-            raise ValueError("seq must be divisible by tp_size")
         if self.granularity < 1:
             raise ValueError("granularity must be >= 1")
         if self.reps < 1:
             raise ValueError("reps must be >= 1")
+        if self.seq % (t * self.granularity):
+            raise ValueError(f"seq ({self.seq}) must be divisible by tp_size*granularity ({t * self.granularity})")
         if self.delay_ms != 0.0:
             raise ValueError("delay_ms is a CPU-fabric knob; the GPU bench measures real transfers (use 0)")
         if self.layer not in LAYERS:
@@ -78,12 +78,18 @@ class BenchConfig:
         if self.schedule == "pairwise" and t > 1 and t % 2:
             raise ValueError("pairwise schedule needs an even tp_size")
         if self.layer in ("attention", "ulysses"):
-            if self.d_model % self.heads or self.heads % t:
-                raise ValueError("heads must divide d_model and tp_size must divide heads")
+            if self.heads % t:
+                raise ValueError(f"heads ({self.heads}) must be divisible by tp_size ({t})")
+            if self.d_model % self.heads:
+                raise ValueError(f"d_model ({self.d_model}) must be divisible by heads ({self.heads})")
+            if self.granularity != 1:
+                raise ValueError("attention layers support granularity = 1 only")
             if self.d_model // self.heads != 128:
                 raise ValueError("the fused attention kernel needs head_dim = d_model / heads = 128")
-        if self.layer == "mlp" and (2 * self.d_model) % t:
-            raise ValueError("tp_size must divide the MLP hidden size 2*d_model")
+        if self.layer == "mlp" and self.d_model % t:
+            raise ValueError(f"d_model ({self.d_model}) must be divisible by tp_size ({t})")
+        if self.layer in ("mlp", "rs") and self.granularity > 1 and self.schedule != "ring":
+            raise ValueError("fuse_reduce_scatter: granularity > 1 is supported for the ring schedule only")
         if self.layer in ("mlp", "attention", "rs", "ag") and (self.d_model * 2) % 16:
             raise ValueError("d_model rows must be 16-byte aligned in bf16 (d_model % 8 == 0)")
 
@@ -210,7 +216,7 @@ def make_setup(cfg: BenchConfig):
             make_slice = slice_gemm
 
             def settle(ib):
-                torch.stack(ib).sum(1, out=outs["data-slicing"])
+                torch.sum(torch.stack(ib), 1, out=outs["data-slicing"])
 
             _sliced_settle(torch, T, side, make_slice, inbox, settle)
 
@@ -224,18 +230,22 @@ def make_setup(cfg: BenchConfig):
         return st
 
     if cfg.layer == "ag":
-        # experiment.cpp:718-739: each rank's (B,S/T,D) slice in [0,3), identity compute;
-        # baseline and data-slicing are both the plain all-gather.
+        # experiment.cpp:718-739: each rank's (B,S/T,D) slice in [0,3); baseline and
+        # data-slicing are both the plain all-gather. The fused path's partial compute is a
+        # GEMM, so f = matmul(I) here, and the two conventional arms apply the same f after
+        # their all-gather so that all three compute the same function.
         xin = torch.stack([_randint(torch, (B, sl, D), 0, 3, seed * 1000 + q, dev) for q in range(T)])
         eye = torch.eye(D, device=dev, dtype=torch.bfloat16).expand(T, D, D).contiguous()
         outs = {s: torch.empty((T, B, S, D), device=dev, dtype=torch.float32) for s in STRATEGIES}
         comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, B, S, D, D, cfg.granularity))
         st.comm = comm
 
+        gathered = torch.empty((T, B * S, D), device=dev, dtype=torch.bfloat16)
+
         def gather(name):
             def run():
-                full = xin.permute(1, 0, 2, 3).reshape(B, S, D)
-                outs[name].copy_(full.unsqueeze(0).expand(T, B, S, D))
+                gathered.view(T, B, S, D).copy_(xin.permute(1, 0, 2, 3).reshape(B, S, D).unsqueeze(0))
+                outs[name].view(T, B * S, D).copy_(torch.bmm(gathered, eye, out_dtype=torch.float32))
             return run
 
         st.body = {"baseline": gather("baseline"), "data-slicing": gather("data-slicing"),
@@ -274,7 +284,7 @@ def make_setup(cfg: BenchConfig):
                 return torch.matmul(ctx, w_o.unsqueeze(1)).float()
 
             _sliced_settle(torch, T, side, make_slice, inbox,
-                           lambda ib: torch.stack(ib).sum(1, out=outs["data-slicing"]))
+                           lambda ib: torch.sum(torch.stack(ib), 1, out=outs["data-slicing"]))
 
         st.body = {"baseline": baseline, "data-slicing": sliced,
                    "fused": lambda: comm.query_split_attention(q, k, v, w_o, outs["fused"], B, h, kind=kind)}
@@ -282,7 +292,7 @@ def make_setup(cfg: BenchConfig):
     else:  # ulysses, experiment.cpp:644-691
         F = T * h * Dh
         outs = {s: torch.empty((T, B, sl, F), device=dev, dtype=torch.bfloat16) for s in STRATEGIES}
-        comm = tpf.Communicator.local_group(T, 1 << 26)
+        comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, B, cfg.heads, S, Dh))
         st.comm = comm
 
         def a2a_into(out, ctx_slices):

@@ -37,7 +37,11 @@ def test_latency_reduction_against_first_strategy():
     ({"seq": 63}, "divisible"), ({"granularity": 0}, "granularity"), ({"reps": 0}, "reps"),
     ({"layer": "conv"}, "layer"), ({"schedule": "tree"}, "schedule"),
     ({"schedule": "pairwise", "tp_size": 3, "seq": 63}, "even"),
-    ({"layer": "attention", "d_model": 32}, "head_dim"), ({"delay_ms": 1.0}, "delay_ms")])
+    ({"layer": "attention", "d_model": 32}, "head_dim"), ({"delay_ms": 1.0}, "delay_ms"),
+    ({"seq": 64, "granularity": 32}, "tp_size\\*granularity"),
+    ({"layer": "attention", "d_model": 512, "granularity": 2}, "granularity = 1"),
+    ({"layer": "ulysses", "heads": 6, "d_model": 768}, "heads \\(6\\) must be divisible"),
+    ({"layer": "rs", "granularity": 2, "schedule": "pairwise"}, "ring schedule only")])
 def test_validate_rejects(kw, msg):
     with pytest.raises(ValueError, match=msg):
         bc.BenchConfig(**kw).validate()
@@ -71,7 +75,8 @@ def test_rows_match_reference_run_bench(layer):
 @pytest.mark.gpu
 @pytest.mark.parametrize("kw", [
     {"layer": "mlp"},                                   # the reference's desk config
-    {"layer": "rs", "schedule": "pairwise", "granularity": 2},
+    {"layer": "rs", "granularity": 2},
+    {"layer": "rs", "schedule": "pairwise"},
     {"layer": "ag", "granularity": 2},
     {"layer": "mlp", "tp_size": 4, "batch": 1, "seq": 2048, "d_model": 1024, "schedule": "circular-slices"},
     {"layer": "attention", "tp_size": 2, "batch": 1, "seq": 512, "d_model": 512, "heads": 4},
