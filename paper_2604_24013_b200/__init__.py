@@ -16,7 +16,8 @@ from dataclasses import dataclass
 from typing import Optional, Sequence
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtpfuse_b200.so")
+# TPF_LIB_PATH: an alternative build of the same library (dev A/B experiments only)
+LIB_PATH = os.environ.get("TPF_LIB_PATH") or os.path.join(_HERE, "libtpfuse_b200.so")
 
 RING, PAIRWISE, CIRCULAR = 0, 1, 2
 KIND_NAMES = {RING: "ring", PAIRWISE: "pairwise", CIRCULAR: "circular-slices"}

@@ -43,6 +43,59 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
+// Packed fp32x2 helpers (FFMA2 / FADD2 on sm_100a).
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2_split(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x for a pair of x <= 0 on the FMA pipe (offloads the MUFU unit): x = j + f with j the
+// nearest integer (1.5 * 2^23 rounding trick), 2^f by a degree-3 minimax polynomial on
+// [-0.5, 0.5] (max rel. error 7.5e-5, far below the bf16 rounding of P), 2^j added into the
+// exponent field. x is clamped at -127, where the result is below bf16's smallest normal.
+__device__ __forceinline__ float2 exp2_poly2(float x0, float x1) {
+  const uint64_t x = f2(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t t = f2_add(x, f2(12582912.f, 12582912.f));
+  const uint64_t j = f2_add(t, f2(-12582912.f, -12582912.f));
+  const uint64_t fr = f2_fma(j, f2(-1.f, -1.f), x);
+  uint64_t pp = f2_fma(fr, f2(0.0551716685f, 0.0551716685f), f2(0.242611155f, 0.242611155f));
+  pp = f2_fma(pp, fr, f2(0.693260968f, 0.693260968f));
+  pp = f2_fma(pp, fr, f2(0.999928057f, 0.999928057f));
+  const float2 pv = f2_split(pp), tv = f2_split(t);
+  return make_float2(__int_as_float(__float_as_int(pv.x) + (__float_as_int(tv.x) << 23)),
+                     __int_as_float(__float_as_int(pv.y) + (__float_as_int(tv.y) << 23)));
+}
+
+// Exps per 8-element P chunk computed on the FMA pipe instead of MUFU (pairs, 0..4).
+#ifndef TPF_POLY_PAIRS
+#define TPF_POLY_PAIRS 1
+#endif
+constexpr int kPolyPairs = TPF_POLY_PAIRS;
+// Keep a stale running max until the new one exceeds it by this much (log2 units): exps stay
+// <= 2^8 and O is rescaled only on a large jump, never on the small moves of later blocks.
+constexpr float kRescaleThreshold = 8.0f;
+
 __device__ __forceinline__ void fmha_wait(const FmhaParams& p, uint64_t* bar, uint32_t parity) {
   if (mbar_try_wait(bar, parity)) return;
   const uint64_t t0 = globaltimer();
@@ -242,12 +295,14 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
 #pragma unroll
           for (int q = 0; q < 2; ++q)
 #pragma unroll
-            for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(s[q][i]));
+            for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(s[q][i]), __uint_as_float(s[q][i + 1]));
         }
-        // raw-score max (scale > 0): exp2(s * scale - mx * scale) in one FFMA per element
-        const float alpha = (m == -INFINITY) ? 0.f : fast_exp2((m - mx) * scale);
-        const float neg = -mx * scale;
-        float rs = 0.f;
+        // Raw-score max (scale > 0). Keep the stale max unless it grew past the threshold.
+        const bool moved = m == -INFINITY || (mx - m) * scale > kRescaleThreshold;
+        const float mu = moved ? mx : m;
+        const float alpha = (m == -INFINITY) ? 0.f : (moved ? fast_exp2((m - mx) * scale) : 1.f);
+        const uint64_t sc2 = f2(scale, scale), neg2 = f2(-mu * scale, -mu * scale);
+        uint64_t rs2a = f2(0.f, 0.f), rs2b = f2(0.f, 0.f);
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass) {
           const int half = 1 - pass;  // columns 64..127 are resident, then 0..63
@@ -263,10 +318,19 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
               uint32_t pk[4];
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float a = fast_exp2(fmaf(__uint_as_float(s[q][cc * 8 + 2 * e]), scale, neg));
-                const float b = fast_exp2(fmaf(__uint_as_float(s[q][cc * 8 + 2 * e + 1]), scale, neg));
-                rs += a + b;
-                pk[e] = pack_bf16x2(a, b);
+                const int i = cc * 8 + 2 * e;
+                // exp2(s * scale - mu * scale), one FFMA2 per pair
+                const float2 x = f2_split(f2_fma(f2(__uint_as_float(s[q][i]), __uint_as_float(s[q][i + 1])), sc2, neg2));
+                float2 y;
+                if (e >= 4 - kPolyPairs) {
+                  y = exp2_poly2(x.x, x.y);
+                } else {
+                  y.x = fast_exp2(x.x);
+                  y.y = fast_exp2(x.y);
+                }
+                if (e & 1) rs2b = f2_add(rs2b, f2(y.x, y.y));
+                else rs2a = f2_add(rs2a, f2(y.x, y.y));
+                pk[e] = pack_bf16x2(y.x, y.y);
               }
               // P row -> SMEM, SWIZZLE_128B K-major image: atom = kv / 64, 16 B chunk ^ (row & 7)
               const int chunk = q * 4 + cc;
@@ -275,6 +339,8 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
             }
           }
         }
+        const float2 ra = f2_split(rs2a), rb = f2_split(rs2b);
+        const float rs = (ra.x + ra.y) + (rb.x + rb.y);
         lsum = lsum * alpha + rs;
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
           // online-softmax correction of the running O (PV_w(j-1) is complete: S_w(j) was
@@ -290,7 +356,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           }
           tmem_st_wait();
         }
-        m = mx;
+        m = mu;
         fence_proxy_async_smem();  // generic SMEM writes of P -> visible to the tensor core
         tc_fence_before();
         __syncwarp();
