@@ -6,16 +6,16 @@
 // One CTA per SM, 12 warps; a work item is a PAIR of 128-row query tiles of one head, so two
 // softmax warpgroups ping-pong against the tensor core:
 //   warp 0      TMA producer: Q0 | Q1 (2 x 128 x 128) per item, then K_j, V_j through a
-//               3-slot ring of 32 KiB tiles
+//               5-slot ring of 32 KiB tiles
 //   warp 1      tcgen05.mma issuer (cta_group::1), per kv block j:
 //                 PV0_{j-1}, S0_j = Q0 K_j^T, PV1_{j-1}, S1_j = Q1 K_j^T
 //               so softmax 0 works on S0_j while the tensor core runs PV1 / S1 and vice versa
 //   warp 2      TMEM allocator (S0 | S1 | O0 | O1: 4 x 128 fp32 columns)
 //   warps 4-7   softmax + epilogue of tile 0, thread = query row
 //   warps 8-11  softmax + epilogue of tile 1
-// Softmax: S row from TMEM, online max/sum (exp2 with the scale folded into one FFMA), P as
-// the bf16 SWIZZLE_128B K-major operand image in SMEM, O rescaled in TMEM only when a row
-// max of the warp moved. Every ordering hazard is covered by MMA issue order: S_w(j+1) is
+// Softmax: S row from TMEM, online max/sum (exp2 with the scale folded into one FFMA2, part
+// of the exps on the FMA pipe), P written back over S in TMEM as packed bf16 (the A operand
+// of the TS-form P.V MMA), O rescaled in TMEM only when a row max jumped past a threshold. Every ordering hazard is covered by MMA issue order: S_w(j+1) is
 // issued after PV_w(j), which waits for P_w(j), so one s_full arrival means "S_w(j+1) ready,
 // and P_w / O_w free". Epilogue: O / l -> bf16 -> peer store + flag.
 // Work items (step i, head g, q-tile pair) run step-major, so the rank's own slice (step
@@ -34,8 +34,8 @@ namespace {
 constexpr int kFTile = 128;                          // q rows / kv rows per tile, head_dim
 constexpr int kFAtom = kFTile * 64 * 2;              // one 64-column SW128 atom: 16 KiB
 constexpr int kFTileBytes = 2 * kFAtom;              // one 128 x 128 bf16 tile: 32 KiB
-constexpr int kFRing = 3;                            // K/V ring slots
-constexpr int kFSmem = (2 + kFRing + 2) * kFTileBytes + 1024 + 256;  // Q0 Q1 | ring | P0 P1
+constexpr int kFRing = 5;                            // K/V ring slots
+constexpr int kFSmem = (2 + kFRing) * kFTileBytes + 1024 + 256;  // Q0 Q1 | ring
 
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
@@ -116,16 +116,15 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sq = smem;                                  // Q0, Q1
   uint8_t* ring = smem + 2 * kFTileBytes;              // kFRing x 32 KiB
-  uint8_t* sp = ring + kFRing * kFTileBytes;           // P0, P1
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sp + 2 * kFTileBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kFRing * kFTileBytes);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* r_full = bars + 2;     // [kFRing]
-  uint64_t* r_empty = bars + 5;    // [kFRing]
-  uint64_t* s_full = bars + 8;     // [2]
-  uint64_t* p_ready = bars + 10;   // [2]
-  uint64_t* pv_done = bars + 12;   // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* r_full = bars + 2;             // [kFRing]
+  uint64_t* r_empty = bars + 2 + kFRing;   // [kFRing]
+  uint64_t* s_full = bars + 2 + 2 * kFRing;   // [2]
+  uint64_t* p_ready = s_full + 2;             // [2]
+  uint64_t* pv_done = s_full + 4;             // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int h = blockIdx.x / p.ctas_per_rank;
@@ -161,7 +160,14 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;  // S0 @ 0, S1 @ 128, O0 @ 256, O1 @ 384
+  // Register split: warps 0-3 (TMA, MMA, TMEM) need few, the softmax warpgroups hold a whole
+  // 128-wide S row: 72 * 128 + 216 * 256 = 168 * 384, exactly the pool the CTA launched with.
+  // setmaxnreg.inc blocks until the pool can satisfy it, so the sum must not exceed the pool
+  // (checked at launch). Each warpgroup executes one setmaxnreg at the top of its branch, so
+  // ptxas allocates the branch under that limit.
 
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 72;");
   if (warp == 0) {
     // =============================================================== TMA producer
     if (lane == 0) {
@@ -194,12 +200,11 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
     }
   } else if (warp == 1) {
     // =============================================================== MMA issuer
-    if (lane == 0) {
+    {  // the whole warp runs the loop (uniform values); elect.sync issues
       constexpr uint32_t idesc_s = make_idesc_bf16(kFTile, kFTile, /*b_mn_major=*/false);
       constexpr uint32_t idesc_o = make_idesc_bf16(kFTile, kFTile, /*b_mn_major=*/true);
       uint32_t rc = 0, ic = 0, pc = 0;
       const uint32_t qa = smem_u32(sq);
-      const uint32_t pa = smem_u32(sp);
       auto ring_wait = [&](uint32_t idx) {
         fmha_wait(p, r_full + idx % kFRing, (idx / kFRing) & 1);
         tc_fence_after();
@@ -210,18 +215,17 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
 #pragma unroll
         for (int k = 0; k < kFTile / 16; ++k) {
           const uint32_t off = (k >> 2) * kFAtom + (k & 3) * 32;
-          mma_bf16(tmem + w * kFTile, make_sdesc(q + off, 0, 1024), make_sdesc(ka + off, 0, 1024), idesc_s, k > 0);
+          mma_bf16_warp(tmem + w * kFTile, make_sdesc(q + off, 0, 1024), make_sdesc(ka + off, 0, 1024), idesc_s, k > 0);
         }
-        mma_commit(s_full + w);
+        mma_commit_warp(s_full + w);
       };
       auto issue_pv = [&](int w, uint32_t va, bool acc) {
-        const uint32_t pw = pa + w * kFTileBytes;
 #pragma unroll
         for (int k = 0; k < kFTile / 16; ++k) {
-          // A = P (K-major over kv), B = V (MN-major: rows kv, 64-col atoms 16 KiB apart)
-          const uint64_t ad = make_sdesc(pw + (k >> 2) * kFAtom + (k & 3) * 32, 0, 1024);
+          // A = P from TMEM (S_w's first 64 columns, 16 kv per 8 columns), B = V (MN-major:
+          // rows kv, 64-col atoms 16 KiB apart)
           const uint64_t bd = make_sdesc(va + k * 2048, kFAtom, 1024);
-          mma_bf16(tmem + (2 + w) * kFTile, ad, bd, idesc_o, acc || k > 0);
+          mma_bf16_ts_warp(tmem + (2 + w) * kFTile, tmem + w * kFTile + k * 8, bd, idesc_o, acc || k > 0);
         }
       };
       for (int it = c; it < nitems; it += C, ++ic) {
@@ -232,8 +236,8 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           const uint32_t ka = ring_wait(base);
           issue_s(0, ka);
           issue_s(1, ka);
-          mma_commit(r_empty + base % kFRing);
-          if (p.nkv == 1) mma_commit(q_empty);
+          mma_commit_warp(r_empty + base % kFRing);
+          if (p.nkv == 1) mma_commit_warp(q_empty);
         }
         for (int j = 0; j < p.nkv; ++j) {
           const bool more = j + 1 < p.nkv;
@@ -242,7 +246,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           fmha_wait(p, p_ready + 0, pc & 1);
           tc_fence_after();
           issue_pv(0, va, j > 0);
-          if (!more) mma_commit(pv_done + 0);
+          if (!more) mma_commit_warp(pv_done + 0);
           uint32_t ka = 0;
           if (more) {
             ka = ring_wait(kidx);
@@ -252,18 +256,20 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           ++pc;
           tc_fence_after();
           issue_pv(1, va, j > 0);
-          mma_commit(r_empty + vidx % kFRing);
-          if (!more) mma_commit(pv_done + 1);
+          mma_commit_warp(r_empty + vidx % kFRing);
+          if (!more) mma_commit_warp(pv_done + 1);
           if (more) {
             issue_s(1, ka);
-            mma_commit(r_empty + kidx % kFRing);
-            if (j + 2 == p.nkv) mma_commit(q_empty);
+            mma_commit_warp(r_empty + kidx % kFRing);
+            if (j + 2 == p.nkv) mma_commit_warp(q_empty);
           }
         }
         rc = base + 2 * p.nkv;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;");
     // =============================================================== softmax + epilogue
     const int w = (warp - 4) >> 2;          // query tile of the pair
     const int ew = warp & 3;                // TMEM lane quarter
@@ -271,7 +277,6 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
     const uint32_t lane_off = static_cast<uint32_t>(ew * 32) << 16;
     const uint32_t t_s = tmem + lane_off + w * kFTile;
     const uint32_t t_o = tmem + lane_off + (2 + w) * kFTile;
-    uint8_t* spw = sp + w * kFTileBytes;
     const float scale = p.scale_log2;
     uint32_t sc = 0, ic = 0;
     for (int it = c; it < nitems; it += C, ++ic) {
@@ -283,20 +288,29 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       for (int j = 0; j < p.nkv; ++j, ++sc) {
         fmha_wait(p, s_full + w, sc & 1);
         tc_fence_after();
-        // Row max over two halves (64 registers live), then exp/pack/store half by half; the
-        // second half is still in registers, the first is reloaded from TMEM.
-        uint32_t s[2][32];
-        float mx = m;
+        // The whole S row in registers (the softmax warpgroups run with 216 registers), one
+        // TMEM round trip; the row max as a tree of 8 independent FMNMX3 chains.
+        uint32_t s[4][32];
+#ifdef TPF_FMHA_EXPERIMENT_NO_LD  // dev experiment: softmax without the TMEM read
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
-          for (int q = 0; q < 2; ++q) tmem_ld_32x32b_x32(t_s + (half * 2 + q) * 32, s[q]);
-          tmem_ld_wait();
+          for (int i = 0; i < 32; ++i) s[q][i] = __float_as_uint(static_cast<float>(i));
+#else
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
+        for (int q = 0; q < 4; ++q) tmem_ld_32x32b_x32(t_s + q * 32, s[q]);
+        tmem_ld_wait();
+#endif
+        float mxp[8];
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) mx = fmax3(mx, __uint_as_float(s[q][i]), __uint_as_float(s[q][i + 1]));
-        }
+        for (int t = 0; t < 8; ++t) mxp[t] = fmaxf(__uint_as_float(s[t >> 1][(t & 1) * 16]), m);
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+#pragma unroll
+          for (int i = 1; i < 16; i += 2)
+            mxp[t] = fmax3(mxp[t], __uint_as_float(s[t >> 1][(t & 1) * 16 + i]),
+                           __uint_as_float(s[t >> 1][(t & 1) * 16 + ((i + 1) & 15)]));
+        const float mx = fmaxf(fmax3(fmax3(mxp[0], mxp[1], mxp[2]), fmax3(mxp[3], mxp[4], mxp[5]), mxp[6]), mxp[7]);
         // Raw-score max (scale > 0). Keep the stale max unless it grew past the threshold.
         const bool moved = m == -INFINITY || (mx - m) * scale > kRescaleThreshold;
         const float mu = moved ? mx : m;
@@ -304,40 +318,36 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         const uint64_t sc2 = f2(scale, scale), neg2 = f2(-mu * scale, -mu * scale);
         uint64_t rs2a = f2(0.f, 0.f), rs2b = f2(0.f, 0.f);
 #pragma unroll
-        for (int pass = 0; pass < 2; ++pass) {
-          const int half = 1 - pass;  // columns 64..127 are resident, then 0..63
-          if (pass == 1) {
+        for (int q = 0; q < 4; ++q) {
 #pragma unroll
-            for (int q = 0; q < 2; ++q) tmem_ld_32x32b_x32(t_s + q * 32, s[q]);
-            tmem_ld_wait();
-          }
+          uint32_t pq[16];  // 32 probabilities of this chunk, bf16x2 = 16 TMEM columns
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
+          for (int cc = 0; cc < 4; ++cc) {
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = cc * 8 + 2 * e;
-                // exp2(s * scale - mu * scale), one FFMA2 per pair
-                const float2 x = f2_split(f2_fma(f2(__uint_as_float(s[q][i]), __uint_as_float(s[q][i + 1])), sc2, neg2));
-                float2 y;
-                if (e >= 4 - kPolyPairs) {
-                  y = exp2_poly2(x.x, x.y);
-                } else {
-                  y.x = fast_exp2(x.x);
-                  y.y = fast_exp2(x.y);
-                }
-                if (e & 1) rs2b = f2_add(rs2b, f2(y.x, y.y));
-                else rs2a = f2_add(rs2a, f2(y.x, y.y));
-                pk[e] = pack_bf16x2(y.x, y.y);
+            for (int e = 0; e < 4; ++e) {
+              const int i = cc * 8 + 2 * e;
+              // exp2(s * scale - mu * scale), one FFMA2 per pair
+              const float2 x = f2_split(f2_fma(f2(__uint_as_float(s[q][i]), __uint_as_float(s[q][i + 1])), sc2, neg2));
+              float2 y;
+#ifdef TPF_FMHA_EXPERIMENT_NO_EXP  // dev experiment: softmax without the exponentials
+              if (true) {
+                y = x;
+              } else
+#endif
+              if (e >= 4 - kPolyPairs) {
+                y = exp2_poly2(x.x, x.y);
+              } else {
+                y.x = fast_exp2(x.x);
+                y.y = fast_exp2(x.y);
               }
-              // P row -> SMEM, SWIZZLE_128B K-major image: atom = kv / 64, 16 B chunk ^ (row & 7)
-              const int chunk = q * 4 + cc;
-              *reinterpret_cast<uint4*>(spw + half * kFAtom + row * 128 + ((chunk ^ (row & 7)) << 4)) =
-                  make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              if (e & 1) rs2b = f2_add(rs2b, f2(y.x, y.y));
+              else rs2a = f2_add(rs2a, f2(y.x, y.y));
+              pq[cc * 4 + e] = pack_bf16x2(y.x, y.y);
             }
           }
+          // P overwrites S_w in place (columns q*16 .. q*16+15: already read into registers);
+          // S_w(j+1) is issued only after PV_w(j) has consumed it
+          tmem_st_32x32b_x16(t_s + q * 16, pq);
         }
         const float2 ra = f2_split(rs2a), rb = f2_split(rs2b);
         const float rs = (ra.x + ra.y) + (rb.x + rb.y);
@@ -357,7 +367,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           tmem_st_wait();
         }
         m = mu;
-        fence_proxy_async_smem();  // generic SMEM writes of P -> visible to the tensor core
+        tmem_st_wait();  // P in TMEM before the tensor core may read it
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_ready + w);
@@ -407,13 +417,20 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-void launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream) {
+cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tpf_fmha_a2a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, tpf_fmha_a2a_kernel);
+    if (e != cudaSuccess) return e;
+    // the setmaxnreg split above must fit the pool the launch allocates, or the kernel hangs
+    if (fa.numRegs * 384 < 72 * 128 + 216 * 256) return cudaErrorInvalidConfiguration;
+    e = cudaFuncSetAttribute(tpf_fmha_a2a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
   tpf_fmha_a2a_kernel<<<grid, 384, kFSmem, stream>>>(p);
+  return cudaGetLastError();
 }
 
 }  // namespace tpf

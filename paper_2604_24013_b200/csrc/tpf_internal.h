@@ -138,7 +138,7 @@ struct UlyssesParams {
 
 void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream);
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
-void launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
 void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
                        int rank, cudaStream_t st);

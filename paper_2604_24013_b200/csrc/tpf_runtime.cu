@@ -695,8 +695,7 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* q, const void* k, const 
   fp.timeout_ns = c->timeout_ns;
   const int sms = tpf::num_sms();
   fp.ctas_per_rank = std::max(1, sms / R);
-  tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
-  TPF_CUDA_TRY_STATUS(cudaGetLastError());
+  TPF_CUDA_TRY_STATUS(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
   for (int hh = 0; hh < R; ++hh) {
     const int rank = r0 + hh;
     uint32_t* f = flags_at(rank);
@@ -858,8 +857,7 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   fp.fault_rank = -1;
   const int sms = tpf::num_sms();
   fp.ctas_per_rank = std::max(1, sms / R);
-  tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream);
-  TPF_CUDA_TRY(cudaGetLastError());
+  TPF_CUDA_TRY(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
   Call kc{};
   kc.op = tpf::OP_RS;
   kc.T = T;
