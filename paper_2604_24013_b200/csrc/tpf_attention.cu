@@ -89,7 +89,7 @@ __device__ __forceinline__ float2 exp2_poly2(float x0, float x1) {
 
 // Exps per 8-element P chunk computed on the FMA pipe instead of MUFU (pairs, 0..4).
 #ifndef TPF_POLY_PAIRS
-#define TPF_POLY_PAIRS 1
+#define TPF_POLY_PAIRS 0
 #endif
 constexpr int kPolyPairs = TPF_POLY_PAIRS;
 // Keep a stale running max until the new one exceeds it by this much (log2 units): exps stay
@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   uint64_t* pv_done = s_full + 4;             // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + 6);
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const int h = blockIdx.x / p.ctas_per_rank;
   const int c = blockIdx.x - h * p.ctas_per_rank;
   if (h >= p.R) return;
