@@ -295,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   uint64_t* fwd_ready = bars + 2 * kStages + 4;  // [2][kStages]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kStages + 4);
 
-  const int warp = threadIdx.x >> 5;
+  // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
   const int lane = threadIdx.x & 31;
   const int cta = static_cast<int>(cluster_ctarank());
   const bool leader = cta == 0;

@@ -105,17 +105,17 @@ def main():
     o = torch.empty((T, 1, S // T, T * heads * Dh), device=DEV, dtype=torch.bfloat16)
     comm = tpf.Communicator.local_group(T, 1 << 27)
     flops = 4.0 * T * heads * S * S * Dh  # whole group: QK^T + PV, non-causal
-    t = timeit(lambda: comm.attention_a2a(q, k, v, o, 1, heads), n=1, warm=1, reps=2)
+    t = timeit(lambda: comm.attention_a2a(q, k, v, o, 1, heads), n=2, warm=2, reps=3)
     comm.sync()
     comm.close()
     C["cfg5_up_T8_S32768"] = {"ms": round(t, 3), "tflops": round(flops / (t * 1e-3) / 1e12, 1),
-                              "note": "v2: one persistent tcgen05 flash-attention launch (S, O in TMEM, P in SMEM) "
-                                      "whose epilogue pushes O tiles to the slice owner + flags"}
+                              "note": "one persistent tcgen05 flash-attention launch (two query tiles per CTA, S/P/O in "
+                                      "TMEM) whose epilogue pushes O tiles to the slice owner + flags"}
     # cfg5 end to end: sequence-sharded q/k/v -> first all-to-all -> fused attention -> output a2a
     H = T * heads
     qs, ks, vs = (rnd((T, H, S // T, Dh), 1.0, 20 + i) for i in range(3))
     comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, 1, H, S, Dh))
-    t_full = timeit(lambda: comm.ulysses_attention(qs, ks, vs, o, 1, H), n=1, warm=1, reps=2)
+    t_full = timeit(lambda: comm.ulysses_attention(qs, ks, vs, o, 1, H), n=2, warm=2, reps=3)
     hq, hk, hv = (torch.empty((T, heads, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3))
     t_a2a = timeit(lambda: comm.ulysses_a2a(qs, ks, vs, hq, hk, hv, 1, H), n=3, warm=1, reps=3)
     comm.sync()
