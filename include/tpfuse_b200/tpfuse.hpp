@@ -338,6 +338,23 @@ inline void fuse_all_to_all_attention(RankEndpoint& ep, const void* q, const voi
   detail::check(tpf_attention_a2a(ep.handle(), q, k, v, out, batch, heads, S, Dh, scale_scores ? 1 : 0, stream));
 }
 
+// Ulysses first all-to-all (ref_all_to_all of fabric.cpp:183-207 as layers_test.cpp:347-397
+// drives it): q/k/v (batch*heads_total, S/T, Dh) sequence-sharded -> (batch*heads_total/T, S, Dh).
+inline void ulysses_all_to_all(RankEndpoint& ep, const void* q, const void* k, const void* v, void* q_out,
+                               void* k_out, void* v_out, int64_t batch, int64_t heads_total, int64_t S, int64_t Dh,
+                               cudaStream_t stream = nullptr) {
+  detail::check(tpf_ulysses_a2a(ep.handle(), q, k, v, q_out, k_out, v_out, batch, heads_total, S, Dh, stream));
+}
+
+// The whole UP attention from the sequence-sharded layout: first all-to-all + fused attention
+// with the output all-to-all. out (batch, S/T, heads_total*128) bf16.
+inline void ulysses_attention(RankEndpoint& ep, const void* q, const void* k, const void* v, void* out,
+                              int64_t batch, int64_t heads_total, int64_t S, bool scale_scores = true,
+                              cudaStream_t stream = nullptr) {
+  detail::check(tpf_ulysses_attention(ep.handle(), q, k, v, out, batch, heads_total, S, 128, scale_scores ? 1 : 0,
+                                      stream));
+}
+
 // query_split_attention (layers.hpp:88-91): w_o is this rank's (heads*128, D) row shard.
 inline void query_split_attention(RankEndpoint& ep, const void* q, const void* k, const void* v, const void* w_o,
                                   DeviceTensor& out, int64_t batch, int64_t heads, int64_t S,
