@@ -320,7 +320,6 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         uint64_t rs2a = f2(0.f, 0.f), rs2b = f2(0.f, 0.f);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-#pragma unroll
           uint32_t pq[16];  // 32 probabilities of this chunk, bf16x2 = 16 TMEM columns
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
