@@ -674,3 +674,21 @@ def test_ulysses_rejects_bad_shapes():
         small.ulysses_attention(q, q, q, o, 1, 4)
     comm.close()
     small.close()
+
+
+def test_ulysses_first_a2a_full_cfg5_exact():
+    """cfg5 size (T = 8, 32 heads x 128, S = 32768): the first all-to-all is pure data movement,
+    so it must equal the torch permutation exactly (size-independent property)."""
+    T, H, S, Dh = 8, 32, 32768, 128
+    sl, hl = S // T, H // T
+    g = torch.Generator(device=DEV).manual_seed(5)
+    xs = [torch.randn((T, H, sl, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
+    outs = [torch.empty((T, hl, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3)]
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, 1, H, S, Dh))
+    comm.ulysses_a2a(*xs, *outs, 1, H)
+    comm.sync()
+    comm.close()
+    for x, o in zip(xs, outs):
+        # x[src, g*hl + h, i] -> o[g, h, src*sl + i]
+        want = x.view(T, T, hl, sl, Dh).permute(1, 2, 0, 3, 4).reshape(T, hl, S, Dh)
+        assert torch.equal(o, want)
