@@ -7,7 +7,7 @@
 //   src row (b*H + g*hl + hh, s)  ->  rank g's row (b*hl + hh, r*sl + s),  s in [0, sl)
 // For a fixed (tensor, b, g, hh) the source block (sl x Dh) and its destination block are both
 // contiguous, so the copy is a list of 3*B*H contiguous blocks per source rank. The blocks are
-// cut into 16 KiB pieces and the persistent grid strides over them with 16-byte loads and peer
+// cut into 64 KiB pieces and the persistent grid strides over them with 16-byte loads and peer
 // stores, destination-rotated (peer r+1 first) so every NVLink port is busy from the start.
 // Each CTA then publishes one flag per (source rank, CTA) to every destination after a system
 // fence; the receiver's wait kernel covers T * ctas flags.
@@ -20,9 +20,11 @@
 namespace tpf {
 namespace {
 
-constexpr int kPieceBytes = 16384;
+constexpr int kPushThreads = 512;
+constexpr int kVec = 8;                                   // 16 B loads in flight per thread
+constexpr int kPieceBytes = kPushThreads * kVec * 16;         // 64 KiB
 
-__global__ void __launch_bounds__(512) ulysses_push_kernel(UlyssesParams p) {
+__global__ void __launch_bounds__(kPushThreads) ulysses_push_kernel(UlyssesParams p) {
   const int hosted = blockIdx.x / p.ctas_per_rank;
   const int cta = blockIdx.x % p.ctas_per_rank;
   const int rank = p.rank0 + hosted;
@@ -47,7 +49,16 @@ __global__ void __launch_bounds__(512) ulysses_push_kernel(UlyssesParams p) {
     const int64_t n = min(static_cast<int64_t>(kPieceBytes), block_bytes - piece * kPieceBytes) / 16;
     const int4* s4 = reinterpret_cast<const int4*>(src);
     int4* d4 = reinterpret_cast<int4*>(dst);
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d4[i] = __ldg(s4 + i);
+    if (n == kPushThreads * kVec) {
+      // all loads first (kVec independent 16 B loads per thread), then the peer stores
+      int4 v[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) v[u] = __ldg(s4 + u * kPushThreads + threadIdx.x);
+#pragma unroll
+      for (int u = 0; u < kVec; ++u) d4[u * kPushThreads + threadIdx.x] = v[u];
+    } else {
+      for (int64_t i = threadIdx.x; i < n; i += kPushThreads) d4[i] = __ldg(s4 + i);
+    }
   }
   __syncthreads();
   if (threadIdx.x < T && rank != p.fault_rank) {
@@ -59,7 +70,7 @@ __global__ void __launch_bounds__(512) ulysses_push_kernel(UlyssesParams p) {
 }  // namespace
 
 void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream) {
-  ulysses_push_kernel<<<p.ctas_per_rank * p.R, 512, 0, stream>>>(p);
+  ulysses_push_kernel<<<p.ctas_per_rank * p.R, kPushThreads, 0, stream>>>(p);
 }
 
 }  // namespace tpf
