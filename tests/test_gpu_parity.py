@@ -692,3 +692,34 @@ def test_ulysses_first_a2a_full_cfg5_exact():
         # x[src, g*hl + h, i] -> o[g, h, src*sl + i]
         want = x.view(T, T, hl, sl, Dh).permute(1, 2, 0, 3, 4).reshape(T, hl, S, Dh)
         assert torch.equal(o, want)
+
+
+@pytest.mark.parametrize("op", ["ulysses_a2a", "ulysses_attention", "attention_a2a"])
+def test_failed_rank_raises_group_error_attention(op):
+    """A rank that stops publishing in the all-to-all paths surfaces as GroupError, and the
+    group recovers for the next call."""
+    T, batch, heads, sl, Dh = 4, 1, 4, 128, 128
+    S = sl * T
+    g = torch.Generator(device=DEV).manual_seed(3)
+    xs = [torch.randn((T, batch * heads, sl, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
+    hs = [torch.randn((T, batch * heads // T, S, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
+    outs = [torch.empty((T, batch * heads // T, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3)]
+    o = torch.empty((T, batch, sl, heads * Dh), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, heads, S, Dh))
+    comm.set_timeout_ms(200)
+
+    def call():
+        if op == "ulysses_a2a":
+            comm.ulysses_a2a(*xs, *outs, batch, heads)
+        elif op == "ulysses_attention":
+            comm.ulysses_attention(*xs, o, batch, heads)
+        else:
+            comm.attention_a2a(*hs, o, batch, heads // T)
+        comm.sync()
+
+    comm.inject_fault(1)
+    with pytest.raises(tpf.GroupError, match="rank"):
+        call()
+    comm.inject_fault(-1)
+    call()
+    comm.close()
