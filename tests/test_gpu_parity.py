@@ -723,3 +723,40 @@ def test_failed_rank_raises_group_error_attention(op):
     comm.inject_fault(-1)
     call()
     comm.close()
+
+
+@pytest.mark.parametrize("T,sl", [(2, 384), (1, 128), (4, 640)])
+def test_attention_a2a_odd_query_tile_count(T, sl):
+    """S/T a multiple of 128 but not of 256: the last query-tile pair has one real tile
+    (the kernel computes and drops the phantom second tile, and publishes no flag for it)."""
+    batch, heads, Dh = 1, 2, 128
+    S = sl * T
+    rng = np.random.default_rng(1200 + T)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, (T, batch * heads, S, Dh))) for _ in range(3))
+    want = O.attention_a2a(T, batch, heads, q, k, v, True)
+    dq, dk, dv = (bf16(a).to(DEV) for a in (q, k, v))
+    out = torch.full((T, batch, sl, T * heads * Dh), float("nan"), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, 1 << 26)
+    comm.attention_a2a(dq, dk, dv, out, batch, heads)
+    comm.sync()
+    comm.close()
+    got = out.double().cpu().numpy()
+    assert np.isfinite(got).all()
+    assert rel_deviation(got, want) <= 2e-2
+
+
+def test_query_split_odd_query_tile_count():
+    T, batch, heads, sl, Dh, D = 2, 1, 2, 384, 128, 256
+    S = sl * T
+    rng = np.random.default_rng(1300)
+    q, k, v = (bf16_round(rng.uniform(-1, 1, (T, batch * heads, S, Dh))) for _ in range(3))
+    w_o = bf16_round(rng.uniform(-1, 1, (T * heads * Dh, D)) / 16)
+    dq, dk, dv = (bf16(a).to(DEV) for a in (q, k, v))
+    dw = bf16(w_o.reshape(T, heads * Dh, D)).to(DEV)
+    out = torch.empty((T, batch, sl, D), device=DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, batch, S, heads * Dh, D, 1) + (1 << 22))
+    comm.query_split_attention(dq, dk, dv, dw, out, batch, heads)
+    comm.sync()
+    comm.close()
+    want = O.query_split_attention(T, tpf.RING, batch, heads, q, k, v, w_o)
+    assert rel_deviation(out.double().cpu().numpy(), want) <= 2e-2
