@@ -10,6 +10,7 @@ For each fused op it reports time, TFLOP/s, and exposed comm = fused - compute-o
 import json
 import math
 import os
+import statistics
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -36,15 +37,32 @@ def timeit(fn, n=5, warm=2, reps=3):
     return best  # ms
 
 
-def fused_and_exposed(comm, fn, flops):
-    t = timeit(fn)
-    if comm.world > 1:
-        comm.set_compute_only(True)
-        c = timeit(fn)
-        comm.set_compute_only(False)
-    else:
-        c = t
+def _one(fn):
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1)
+
+
+def fused_and_exposed(comm, fn, flops, rounds=7):
+    """Single calls, fused and compute-only ALTERNATING (so power-cap clock drift lands on
+    both equally); medians. Back-to-back timing swings by 10-20% on these boxes as the
+    power cap engages, which swamps the effect being measured."""
+    for _ in range(2):
+        fn()
+    fused, co = [], []
+    for _ in range(rounds):
+        fused.append(_one(fn))
+        if comm.world > 1:
+            comm.set_compute_only(True)
+            co.append(_one(fn))
+            comm.set_compute_only(False)
     comm.sync()
+    t = statistics.median(fused)
+    c = statistics.median(co) if co else t
     return {"ms": round(t, 4), "tflops": round(flops / (t * 1e-3) / 1e12, 1),
             "compute_only_ms": round(c, 4), "exposed_us": round(1e3 * (t - c), 1)}
 
@@ -74,7 +92,8 @@ def ag_rs(T, S, K_ag, N_ag, K_rs, N_rs, wire=tpf.BF16, out_f32=False):
 def main():
     out_path = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/configs.json"
     res = {"note": "T=1: single-GPU path. T>1: single-GPU local group (T ranks in one launch, 148/T SMs each, "
-                   "wire via local HBM, not NVLink). exposed_us = fused - compute-only.", "configs": {}}
+                   "wire via local HBM, not NVLink). exposed_us = fused - compute-only, medians of single calls "
+                   "with fused / compute-only alternating.", "configs": {}}
     C = res["configs"]
     # cfg1: CPU-reference config (T=4, M=K=N=4096), fp32 wire / output as the parity config
     C["cfg1_T4_4096cubed_fp32"] = ag_rs(4, 4096, 4096, 4096, 4096, 4096, wire=tpf.F32, out_f32=True)

@@ -17,7 +17,7 @@ op = sys.argv[1] if len(sys.argv) > 1 else "ag"
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 kind = int(sys.argv[3]) if len(sys.argv) > 3 else tpf.RING
 wire = int(sys.argv[4]) if len(sys.argv) > 4 else tpf.BF16
-S, D, F = 8192, 4096, 14336
+S, D, F = (int(os.environ.get(k, v)) for k, v in (("TR_S", "8192"), ("TR_D", "4096"), ("TR_F", "14336")))
 g = torch.Generator(device=dev).manual_seed(0)
 if op == "ag":
     x = torch.randn((T, 1, S // T, D), device=dev, generator=g).to(torch.bfloat16)
