@@ -178,9 +178,11 @@ int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local);
  *   q, k, v : bf16 (batch*heads, S, Dh)
  *   out     : bf16 (batch, S/T, T*heads*Dh) = concat_feat over source rank of merge_heads
  * Iteration i computes query slice l = (r+i+1) % T (softmax(q k^T * scale) v, scale =
- * 1/sqrt(Dh) if `scale`) on the tcgen05 GEMM family; the P.V epilogue pushes every output
- * tile straight into rank l's buffer at this rank's feature block and flags it; the own
- * slice is computed last (no trailing transfer). Non-causal, no GQA. */
+ * 1/sqrt(Dh) if `scale`). Dh == 128 with (S/T) % 128 == 0 runs one fused tcgen05
+ * flash-attention launch (S, P, O in TMEM) whose epilogue pushes every output tile straight
+ * into rank l's buffer at this rank's feature block and flags it; other shapes run the GEMM
+ * family (QK^T GEMM, softmax, P.V GEMM with the same push epilogue). The own slice is
+ * computed last (no trailing transfer). Non-causal, no GQA. */
 int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                       int64_t heads, int64_t S, int64_t Dh, int scale, void* stream);
 
