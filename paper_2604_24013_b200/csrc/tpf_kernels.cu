@@ -679,6 +679,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const int64_t orow = ob * p.out_rows + pass * p.Sc + t.row0 + row;
       char* rp = ((kUpEpi && p.out_rank[h]) ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
       for (int j = 0; j < BN / 32; ++j) {
+        // the inbox loads go out before the TMEM read so the two latencies overlap
+        float in[32];
+        if (valid && inbox) wire_load(p.wire_f32, inbox, j, row, in);
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + j * 32, r);
         tmem_ld_wait();
@@ -688,8 +691,6 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         if (valid) {
           if (inbox) {
             // rs_pipelined: partial += inbox   (collectives.cpp:303)
-            float in[32];
-            wire_load(p.wire_f32, inbox, j, row, in);
 #pragma unroll
             for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
           } else if (p.direct && last && p.T > 1 && !p.compute_only) {
