@@ -380,6 +380,29 @@ inline void dp_param_all_gather_gemm(RankEndpoint& ep, const void* x, const void
 }
 
 // ------------------------------------------ single-GPU group (spawn_group analogue)
+// Per-rank attention operands, folded (batch*heads, seq, head_dim): layers.hpp:40-56.
+struct AttentionInputs {
+  int batch = 0;
+  int heads = 0;  // heads held by this rank
+  Tensor q, k, v;
+  int64_t head_dim() const { return q.feat(); }
+  int64_t seq() const { return q.seq(); }
+};
+
+inline AttentionInputs make_attention_inputs(int batch, int heads, Tensor q, Tensor k, Tensor v) {
+  if (batch < 1 || heads < 1) throw std::invalid_argument("attention inputs need batch >= 1 and heads >= 1");
+  if (q.batch() != static_cast<int64_t>(batch) * heads)
+    throw ShapeError("attention inputs: q " + q.shape_str() + " is not folded as (batch*heads, seq, head_dim)");
+  if (!k.same_shape(v) || k.batch() != q.batch() || k.feat() != q.feat())
+    throw ShapeError("attention inputs: k " + k.shape_str() + " / v " + v.shape_str() + " do not match q " +
+                     q.shape_str());
+  return AttentionInputs{batch, heads, std::move(q), std::move(k), std::move(v)};
+}
+
+struct AttentionOptions {
+  bool scale_scores = true;  // scale scores by 1/sqrt(head_dim) before the softmax
+};
+
 class LocalGroup {
  public:
   explicit LocalGroup(int world, size_t sym_bytes_per_rank = size_t(64) << 20) : world_(world) {
@@ -464,7 +487,91 @@ class LocalGroup {
     return fetch(dout, x0.batch(), x0.seq(), Nop, No);
   }
 
+  // fuse_all_to_all_attention (layers.cpp:174-218) on every rank: qkv[r] is rank r's head
+  // group over the whole sequence; returns (batch, S/T, T*heads*Dh) per rank.
+  std::vector<Tensor> fuse_all_to_all_attention(const std::vector<AttentionInputs>& qkv,
+                                                const AttentionOptions& options = {}) {
+    check_attention(qkv, "fuse_all_to_all_attention");
+    const AttentionInputs& a0 = qkv[0];
+    const int64_t S = a0.seq(), Dh = a0.head_dim();
+    if (S % world_)
+      throw std::invalid_argument("fuse_all_to_all_attention: sequence length " + std::to_string(S) +
+                                  " is not divisible by group size " + std::to_string(world_));
+    void* dq = stage_folded(qkv, 0);
+    void* dk = stage_folded(qkv, 1);
+    void* dv = stage_folded(qkv, 2);
+    const int64_t F = static_cast<int64_t>(world_) * a0.heads * Dh;
+    void* dout = alloc(2 * static_cast<size_t>(world_) * a0.batch * (S / world_) * F);
+    detail::check(tpf_attention_a2a(c_, dq, dk, dv, dout, a0.batch, a0.heads, S, Dh, options.scale_scores ? 1 : 0,
+                                    nullptr));
+    detail::check(tpf_comm_sync(c_, nullptr));
+    return fetch_bf16(dout, a0.batch, S / world_, F);
+  }
+
+  // query_split_attention (layers.cpp:149-172): out_proj is row-sharded ((T*heads*Dh) x D).
+  std::vector<Tensor> query_split_attention(const std::vector<AttentionInputs>& qkv, const ShardedLinear& out_proj,
+                                            const Schedule& schedule, const AttentionOptions& options = {}) {
+    check_attention(qkv, "query_split_attention");
+    require_kind(out_proj, ShardedLinear::Kind::RowShard, "query_split_attention");
+    const AttentionInputs& a0 = qkv[0];
+    const int64_t S = a0.seq(), Dh = a0.head_dim(), D = out_proj.shard(0).cols(), Dp = up8(D);
+    if (out_proj.shard(0).rows() != a0.heads * Dh)
+      throw ShapeError("query_split_attention: out_proj shard rows do not match heads * head_dim");
+    void* dq = stage_folded(qkv, 0);
+    void* dk = stage_folded(qkv, 1);
+    void* dv = stage_folded(qkv, 2);
+    void* dw = stage_w(out_proj, a0.heads * Dh, Dp, 0, a0.heads * Dh);
+    float* dout = static_cast<float*>(alloc(sizeof(float) * world_ * a0.batch * (S / world_) * Dp));
+    detail::check(tpf_query_split_attention(c_, dq, dk, dv, dw, dout, a0.batch, a0.heads, S, Dh, Dp,
+                                            static_cast<int>(schedule.kind), TPF_F32, TPF_F32,
+                                            options.scale_scores ? 1 : 0, nullptr));
+    detail::check(tpf_comm_sync(c_, nullptr));
+    return fetch(dout, a0.batch, S / world_, Dp, D);
+  }
+
  private:
+  void check_attention(const std::vector<AttentionInputs>& qkv, const char* op) const {
+    if (static_cast<int>(qkv.size()) != world_)
+      throw std::invalid_argument(std::string(op) + ": expected one input per rank");
+    for (const AttentionInputs& a : qkv)
+      if (a.batch != qkv[0].batch || a.heads != qkv[0].heads || !a.q.same_shape(qkv[0].q) ||
+          !a.k.same_shape(qkv[0].k))
+        throw ShapeError(std::string(op) + ": ranks disagree on attention shapes");
+  }
+
+  // rank-stacked bf16 (T, batch*heads, S, Dh) of q (which = 0), k (1) or v (2)
+  void* stage_folded(const std::vector<AttentionInputs>& qkv, int which) {
+    const Tensor& t0 = which == 0 ? qkv[0].q : which == 1 ? qkv[0].k : qkv[0].v;
+    const size_t n = t0.raw().size();
+    std::vector<uint16_t> h(static_cast<size_t>(world_) * n);
+    for (int r = 0; r < world_; ++r) {
+      const Tensor& t = which == 0 ? qkv[r].q : which == 1 ? qkv[r].k : qkv[r].v;
+      for (size_t i = 0; i < n; ++i) h[r * n + i] = detail::to_bf16(t.raw()[i]);
+    }
+    void* d = alloc(h.size() * 2);
+    detail::cuda_check(cudaMemcpy(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "cudaMemcpy");
+    return d;
+  }
+
+  std::vector<Tensor> fetch_bf16(const void* d, int64_t B, int64_t S, int64_t N) {
+    std::vector<uint16_t> h(static_cast<size_t>(world_ * B * S * N));
+    detail::cuda_check(cudaMemcpy(h.data(), d, h.size() * 2, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    std::vector<Tensor> out;
+    for (int r = 0; r < world_; ++r) {
+      Tensor t(B, S, N);
+      for (int64_t i = 0; i < B * S * N; ++i) {
+        const uint32_t u = static_cast<uint32_t>(h[r * B * S * N + i]) << 16;
+        float f;
+        std::memcpy(&f, &u, 4);
+        t.raw()[i] = f;
+      }
+      out.push_back(std::move(t));
+    }
+    for (void* p : bufs_) cudaFree(p);
+    bufs_.clear();
+    return out;
+  }
+
   static int64_t up8(int64_t v) { return (v + 7) / 8 * 8; }
 
   void require_kind(const ShardedLinear& w, ShardedLinear::Kind k, const char* op) const {

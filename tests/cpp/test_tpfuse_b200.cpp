@@ -6,6 +6,8 @@
 //
 //   test_tpfuse_b200 --cpu   schedule / error tests only (no GPU needed)
 //   test_tpfuse_b200         everything (needs an sm_100 GPU)
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -157,6 +159,57 @@ static void schedule_tests() {
 }
 
 // ------------------------------------------------------------- GPU tests
+// Single-device attention in double (reference_attention, layers.cpp:107-118 semantics):
+// folded (batch*heads, S, Dh), rows [q0, q0+nq) of the queries; returns (batch*heads, nq, Dh).
+static Tensor attention_ref(const Tensor& q, const Tensor& k, const Tensor& v, int64_t q0, int64_t nq, bool scale) {
+  const int64_t G = q.batch(), S = k.seq(), Dh = q.feat();
+  Tensor out(G, nq, Dh);
+  std::vector<double> sc(static_cast<size_t>(S));
+  const double f = scale ? 1.0 / std::sqrt(static_cast<double>(Dh)) : 1.0;
+  for (int64_t g = 0; g < G; ++g)
+    for (int64_t i = 0; i < nq; ++i) {
+      double mx = -1e300;
+      for (int64_t j = 0; j < S; ++j) {
+        double d = 0;
+        for (int64_t c = 0; c < Dh; ++c) d += q(g, q0 + i, c) * k(g, j, c);
+        sc[j] = d * f;
+        mx = std::max(mx, sc[j]);
+      }
+      double sum = 0;
+      for (int64_t j = 0; j < S; ++j) sum += (sc[j] = std::exp(sc[j] - mx));
+      for (int64_t c = 0; c < Dh; ++c) {
+        double a = 0;
+        for (int64_t j = 0; j < S; ++j) a += sc[j] * v(g, j, c);
+        out(g, i, c) = a / sum;
+      }
+    }
+  return out;
+}
+
+static double rel_dev(const Tensor& a, const Tensor& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.raw().size(); ++i) {
+    num = std::max(num, std::fabs(a.raw()[i] - b.raw()[i]));
+    den = std::max(den, std::fabs(b.raw()[i]));
+  }
+  return den > 0 ? num / den : num;
+}
+
+static Tensor uniform_bf16(int64_t b, int64_t s, int64_t d, uint64_t seed) {
+  std::mt19937_64 gen(seed);
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  Tensor t(b, s, d);
+  for (double& x : t.raw()) {
+    float f = static_cast<float>(u(gen));
+    uint32_t bits;
+    std::memcpy(&bits, &f, 4);
+    bits &= 0xffff0000u;  // exactly representable in bf16
+    std::memcpy(&f, &bits, 4);
+    x = f;
+  }
+  return t;
+}
+
 static void gpu_tests() {
   // SPEC acceptance C1: T in {1,2,4,8}, m in {1,2}, every applicable schedule, seeds 0-4,
   // B=2, S=64, D=32, hidden 64; exact equality with the single-device oracle.
@@ -220,6 +273,79 @@ static void gpu_tests() {
                                         ShardedLinear::split_rows(downm, t), Activation::Square,
                                         build_schedule(ScheduleKind::Ring, t));
     for (int r = 0; r < t; ++r) CHECK(out[r] == seq_slice(want, t, r));
+  });
+  // layers_test.cpp FuseAllToAllAttention: rank l receives, from every source rank q,
+  // merge_heads(attention(q's head group, query slice l)) at feature block q.
+  run("Layers.FuseAllToAllAttentionMatchesReference", [] {
+    for (int t : {2, 4})
+      for (int64_t dh : {int64_t(128), int64_t(32)}) {  // fused flash kernel / GEMM family
+        LocalGroup g(t);
+        const int batch = 2, heads = 2;
+        const int64_t S = 128 * t;
+        std::vector<AttentionInputs> in;
+        for (int r = 0; r < t; ++r)
+          in.push_back(make_attention_inputs(batch, heads, uniform_bf16(batch * heads, S, dh, 100 + r),
+                                             uniform_bf16(batch * heads, S, dh, 200 + r),
+                                             uniform_bf16(batch * heads, S, dh, 300 + r)));
+        const auto out = g.fuse_all_to_all_attention(in);
+        const int64_t sl = S / t;
+        for (int l = 0; l < t; ++l) {
+          Tensor want(batch, sl, static_cast<int64_t>(t) * heads * dh);
+          for (int q = 0; q < t; ++q) {
+            const Tensor ctx = attention_ref(in[q].q, in[q].k, in[q].v, l * sl, sl, true);
+            for (int b = 0; b < batch; ++b)
+              for (int hh = 0; hh < heads; ++hh)
+                for (int64_t i = 0; i < sl; ++i)
+                  for (int64_t c = 0; c < dh; ++c)
+                    want(b, i, (static_cast<int64_t>(q) * heads + hh) * dh + c) = ctx(b * heads + hh, i, c);
+          }
+          CHECK(rel_dev(out[l], want) <= 2e-2);
+        }
+      }
+  });
+  // query_split_attention (layers.cpp:149-172): fuse_reduce_scatter of
+  // merge_heads(attention(q_slice)) . W_o[r] over the query sequence, every schedule.
+  run("Layers.QuerySplitAttentionMatchesReference", [] {
+    const int t = 2, batch = 1, heads = 2;
+    const int64_t S = 256 * t, dh = 128, D = 64;
+    LocalGroup g(t);
+    std::vector<AttentionInputs> in;
+    for (int r = 0; r < t; ++r)
+      in.push_back(make_attention_inputs(batch, heads, uniform_bf16(batch * heads, S, dh, 400 + r),
+                                         uniform_bf16(batch * heads, S, dh, 500 + r),
+                                         uniform_bf16(batch * heads, S, dh, 600 + r)));
+    Matrix wo(static_cast<int64_t>(t) * heads * dh, D);
+    {
+      const Tensor w = uniform_bf16(1, t * heads * dh, D, 700);
+      for (int64_t i = 0; i < wo.rows(); ++i)
+        for (int64_t c = 0; c < D; ++c) wo(i, c) = w(0, i, c) / 16;
+    }
+    const ShardedLinear wos = ShardedLinear::split_rows(wo, t);
+    // central: y = sum_r merge_heads(attention_r) . W_o[r], sequence-sliced
+    Tensor y(batch, S, D);
+    for (int r = 0; r < t; ++r) {
+      const Tensor ctx = attention_ref(in[r].q, in[r].k, in[r].v, 0, S, true);
+      for (int b = 0; b < batch; ++b)
+        for (int64_t i = 0; i < S; ++i)
+          for (int64_t c = 0; c < D; ++c) {
+            double a = 0;
+            for (int hh = 0; hh < heads; ++hh)
+              for (int64_t e = 0; e < dh; ++e) a += ctx(b * heads + hh, i, e) * wos.shard(r)(hh * dh + e, c);
+            y(b, i, c) += a;
+          }
+    }
+    for (ScheduleKind k : {ScheduleKind::Ring, ScheduleKind::PairwiseBidirectional, ScheduleKind::CircularSlices}) {
+      const auto out = g.query_split_attention(in, wos, build_schedule(k, t));
+      for (int r = 0; r < t; ++r) CHECK(rel_dev(out[r], seq_slice(y, t, r)) <= 2e-2);
+    }
+  });
+  run("Layers.AttentionErrorBehaviour", [] {
+    LocalGroup g(2);
+    CHECK_THROWS(make_attention_inputs(1, 2, Tensor(3, 8, 8), Tensor(3, 8, 8), Tensor(3, 8, 8)), ShapeError);
+    std::vector<AttentionInputs> in;
+    for (int r = 0; r < 2; ++r)
+      in.push_back(make_attention_inputs(1, 1, Tensor(1, 129, 8), Tensor(1, 129, 8), Tensor(1, 129, 8)));
+    CHECK_THROWS(g.fuse_all_to_all_attention(in), std::invalid_argument);  // 129 % 2
   });
   run("Layers.ErrorBehaviour", [] {
     LocalGroup g(4);
