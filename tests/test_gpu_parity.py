@@ -760,3 +760,30 @@ def test_query_split_odd_query_tile_count():
     comm.close()
     want = O.query_split_attention(T, tpf.RING, batch, heads, q, k, v, w_o)
     assert rel_deviation(out.double().cpu().numpy(), want) <= 2e-2
+
+
+def test_ulysses_attention_full_cfg5_vs_sdpa():
+    """The whole UP layer at cfg 5 size (T = 8, 32 heads x 128, S = 32768; 256 kv blocks per
+    item, so the S/P TMEM aliasing runs through every pipeline phase) vs torch SDPA on the
+    same head groups, checked on the first and last query rows of two slices."""
+    T, batch, H, S, Dh = 8, 1, 32, 32768, 128
+    sl, hl = S // T, H // T
+    g = torch.Generator(device=DEV).manual_seed(21)
+    qs, ks, vs = (torch.randn((T, H, sl, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3))
+    out = torch.empty((T, batch, sl, H * Dh), device=DEV, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, H, S, Dh))
+    comm.ulysses_attention(qs, ks, vs, out, batch, H)
+    comm.sync()
+    comm.close()
+
+    def head_group(x, grp):  # (T_src, H, sl, Dh) -> head group grp over the whole sequence
+        return x[:, grp * hl:(grp + 1) * hl].permute(1, 0, 2, 3).reshape(hl, S, Dh)
+
+    for r in (0, T - 1):
+        rows = torch.cat([torch.arange(0, 64), torch.arange(sl - 64, sl)]).to(DEV)
+        for grp in (0, T - 1):
+            q = head_group(qs, grp)[:, r * sl + rows]
+            ref = torch.nn.functional.scaled_dot_product_attention(q, head_group(ks, grp), head_group(vs, grp))
+            got = out[r, 0][rows][:, grp * hl * Dh:(grp + 1) * hl * Dh].view(-1, hl, Dh).permute(1, 0, 2)
+            err = (got.float() - ref.float()).abs().max().item()
+            assert err <= 2e-2 * ref.float().abs().max().item() + 2e-3, (r, grp, err)
