@@ -199,6 +199,9 @@ int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, vo
 // bf16. Needs Dh == 128 and (S/T) % 128 == 0.
 int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                           int64_t heads_total, int64_t S, int64_t Dh, int scale, void* stream);
+// Symmetric heap bytes per rank that tpf_ulysses_attention, tpf_ulysses_a2a and
+// tpf_attention_a2a (heads = heads_total / world) need; -1 on indivisible shapes.
+int64_t tpf_sym_bytes_ulysses(int world, int64_t batch, int64_t heads_total, int64_t S, int64_t Dh);
 
 /* Query-split attention (Alg. 4). Replaces:
  *   Tensor query_split_attention(RankEndpoint&, const AttentionInputs&, const ShardedLinear& out_proj,

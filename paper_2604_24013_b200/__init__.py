@@ -79,6 +79,8 @@ _lib.tpf_attention_a2a.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
 _lib.tpf_query_split_attention.argtypes = [_vp] * 6 + [_i64] * 5 + [C.c_int] * 4 + [_vp]
 _lib.tpf_ulysses_a2a.argtypes = [_vp] * 7 + [_i64] * 4 + [_vp]
 _lib.tpf_ulysses_attention.argtypes = [_vp] * 5 + [_i64] * 4 + [C.c_int, _vp]
+_lib.tpf_sym_bytes_ulysses.argtypes = [C.c_int] + [_i64] * 4
+_lib.tpf_sym_bytes_ulysses.restype = _i64
 _lib.tpf_sym_bytes_dp_ag.argtypes = [C.c_int, _i64, _i64]
 _lib.tpf_sym_bytes_dp_ag.restype = _i64
 _lib.tpf_swiglu.argtypes = [_vp, _vp, _i64, _i64, _vp]
@@ -113,6 +115,7 @@ EXPORTED_SYMBOLS = (
     "tpf_query_split_attention",
     "tpf_ulysses_a2a",
     "tpf_ulysses_attention",
+    "tpf_sym_bytes_ulysses",
     "tpf_dp_param_ag_gemm",
     "tpf_sym_bytes_dp_ag",
     "tpf_gemm",
@@ -366,11 +369,11 @@ Communicator.ulysses_attention = _ulysses_attention
 
 
 def sym_bytes_ulysses(world, batch, heads, S, Dh=128) -> int:
-    """Symmetric heap bytes per rank for ulysses_attention (and ulysses_a2a)."""
-    sl, hl = S // world, heads // world
-    out_area = batch * sl * heads * Dh * 2
-    inbox = 3 * batch * hl * S * Dh * 2
-    return 2 * (((out_area + 4095) // 4096) * 4096 + inbox) + 2 * (1 << 20) + 8192
+    """Symmetric heap bytes per rank for ulysses_attention / ulysses_a2a / attention_a2a."""
+    n = int(_lib.tpf_sym_bytes_ulysses(world, batch, heads, S, Dh))
+    if n < 0:
+        raise ValueError(f"sym_bytes_ulysses: S={S} / heads={heads} not divisible by world={world}")
+    return n
 
 
 def sym_bytes_dp_ag(world, K, N_local) -> int:

@@ -574,6 +574,16 @@ int64_t tpf_sym_bytes_dp_ag(int world, int64_t K, int64_t N_local) {
   return 2 * kFlagBytesPerParity + 2 * static_cast<int64_t>(world - 1) * slot;
 }
 
+int64_t tpf_sym_bytes_ulysses(int world, int64_t batch, int64_t heads_total, int64_t S, int64_t Dh) {
+  // attention output area (every rank's (batch, S/T, heads_total*Dh) bf16 inbox), then the
+  // first all-to-all inbox [q | k | v] of this rank's head group, per parity
+  if (world < 1 || S % world || heads_total % world) return -1;
+  const int64_t sl = S / world, hl = heads_total / world;
+  const int64_t out_area = batch * sl * heads_total * Dh * 2;
+  const int64_t inbox = 3 * batch * hl * S * Dh * 2;
+  return 2 * (((out_area + 4095) / 4096) * 4096 + inbox) + 2 * kFlagBytesPerParity + 8192;
+}
+
 int64_t tpf_sym_bytes_rs(int world, int64_t B, int64_t S, int64_t K_local, int64_t N, int m,
                          int wire_dtype) {
   if (world <= 1) return 0;
