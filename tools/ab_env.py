@@ -1,5 +1,5 @@
 """Dev tool: the bench block (T = 1, Llama-3-8B MLP) under different environment settings,
-alternating processes. python tests/ab_env.py 'TPF_GROUP_M=16' 'TPF_GROUP_M=32' [rounds]"""
+alternating processes. python tools/ab_env.py 'TPF_GROUP_M=16' 'TPF_GROUP_M=32' [rounds]"""
 import os
 import subprocess
 import sys

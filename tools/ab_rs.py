@@ -1,5 +1,5 @@
 """Dev tool: A/B two library builds on GEMM-RS / AG-GEMM exposed comm (local group),
-alternating processes. python tests/ab_rs.py LIB_A LIB_B [rounds]"""
+alternating processes. python tools/ab_rs.py LIB_A LIB_B [rounds]"""
 import json
 import os
 import subprocess

@@ -1,5 +1,5 @@
 """Dev tool: A/B the UP attention kernel of two library builds in one process pair,
-alternating runs to cancel clock drift. python tests/ab_up.py LIB_A LIB_B [rounds]"""
+alternating runs to cancel clock drift. python tools/ab_up.py LIB_A LIB_B [rounds]"""
 import os
 import subprocess
 import sys

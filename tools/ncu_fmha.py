@@ -1,5 +1,5 @@
 """Dev tool: one cfg5-shaped UP launch for an ncu capture of the fused attention kernel
-(`ncu --set full -k regex:fmha -c 1 python tests/ncu_fmha.py`)."""
+(`ncu --set full -k regex:fmha -c 1 python tools/ncu_fmha.py`)."""
 import os
 import sys
 

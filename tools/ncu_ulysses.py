@@ -1,5 +1,5 @@
 """Dev tool: one cfg5-shaped Ulysses first all-to-all for an ncu capture of the push kernel
-(`ncu --set full -k regex:ulysses -c 1 python tests/ncu_ulysses.py`)."""
+(`ncu --set full -k regex:ulysses -c 1 python tools/ncu_ulysses.py`)."""
 import os
 import sys
 

@@ -5,7 +5,7 @@ in one launch, each on 148/T SMs, wire traffic through local HBM rather than NVL
 For each fused op it reports time, TFLOP/s, and exposed comm = fused - compute-only
 (the same kernel with flag waits and wire traffic disabled).
 
-    python tests/perf_configs.py [out.json]
+    python tools/perf_configs.py [out.json]
 """
 import json
 import math

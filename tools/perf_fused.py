@@ -1,7 +1,7 @@
 """Dev tool: time the fused ops on one GPU (local group = all T ranks in one launch),
 fused vs compute-only (same kernel, no flag waits / wire traffic).
 
-    python tests/perf_fused.py [cfg2|cfg3] [T ...]
+    python tools/perf_fused.py [cfg2|cfg3] [T ...]
 """
 import os
 import sys

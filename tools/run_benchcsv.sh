@@ -1,6 +1,6 @@
 #!/bin/bash
 # Dev / evidence tool: the three-strategy bench in the reference's CSV schema on one B200
-# (single-GPU local group), at BASELINE-sized shapes. Usage: tests/run_benchcsv.sh OUTDIR
+# (single-GPU local group), at BASELINE-sized shapes. Usage: tools/run_benchcsv.sh OUTDIR
 set -e
 out=${1:-gpurun_out}
 mkdir -p "$out"

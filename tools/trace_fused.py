@@ -1,6 +1,6 @@
 """Dev tool: device timeline of one fused call on a single-GPU local group.
 
-    python tests/trace_fused.py ag|rs [T] [kind] [wire]
+    python tools/trace_fused.py ag|rs [T] [kind] [wire]
 """
 import json
 import os
