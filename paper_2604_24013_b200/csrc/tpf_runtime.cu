@@ -174,6 +174,18 @@ int64_t data_bytes_per_parity(size_t sym_bytes) {
   return (static_cast<int64_t>(sym_bytes) - 2 * kFlagBytesPerParity) / 2;
 }
 
+// Multi-rank calls take their epoch (flag value) and heap parity from a host counter, so a
+// captured CUDA graph would replay stale epochs and pass every flag wait on old data.
+// Refuse capture loudly instead (single-rank calls have no flags and may be captured).
+tpf::Status check_not_capturing(const tpf_comm* c, cudaStream_t stream) {
+  if (!c || c->world <= 1) return tpf::Status::ok();
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone)
+    return tpf::Status::invalid("multi-rank fused collectives cannot be captured into a CUDA graph "
+                                "(per-call epochs are host-side); capture only single-rank calls");
+  return tpf::Status::ok();
+}
+
 struct Call {
   int op, T, m, direct, act, wire_f32, out_f32, n_hosted, rank0;
   int64_t B, Sc, K, N, x_rows, out_rows;
@@ -344,6 +356,10 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
       tpf::Status s = make_tmap(&p.tmap_wire, c->sym[k.rank0] + p.data_off[p.parity], 5, dims,
                                 strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
       if (!s.good()) return s;
+    }
+    {
+      const tpf::Status cs = check_not_capturing(c, stream);
+      if (!cs.good()) return cs;
     }
     c->epoch += 1;
     p.epoch = c->epoch;
@@ -748,7 +764,11 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   };
   if (Dh == 128 && sl % 128 == 0) {
     // v2: one persistent fused flash-attention launch for all steps / heads / hosted ranks
-    c->epoch += 1;
+    {
+    const tpf::Status cs = check_not_capturing(c, stream);
+    if (!cs.good()) return fail(cs);
+  }
+  c->epoch += 1;
     s = fmha_a2a_v2(c, q, k, v, static_cast<uint64_t>(G * S * Dh * 2), out, batch, heads, S, c->epoch, scale,
                     stream);
     return s.good() ? TPF_OK : fail(s);
@@ -764,6 +784,10 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   }
   float* scores = reinterpret_cast<float*>(c->scratch);
   char* probs = c->scratch + sc_bytes;
+  {
+    const tpf::Status cs = check_not_capturing(c, stream);
+    if (!cs.good()) return fail(cs);
+  }
   c->epoch += 1;
   const uint32_t epoch = c->epoch;
   const int par = static_cast<int>(epoch & 1u);
@@ -1055,6 +1079,10 @@ int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, vo
   if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
   if (!s.good()) return fail(s);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  {
+    const tpf::Status cs = check_not_capturing(c, stream);
+    if (!cs.good()) return fail(cs);
+  }
   c->epoch += 1;
   char* inbox = nullptr;
   s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, c->epoch, 0, 0, &inbox, stream);
@@ -1078,6 +1106,10 @@ int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void*
   if (Dh != 128 || sl % 128)
     return fail(tpf::Status::shape("tpf_ulysses_attention: the fused path needs head_dim 128 and S/T % 128 == 0"));
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  {
+    const tpf::Status cs = check_not_capturing(c, stream);
+    if (!cs.good()) return fail(cs);
+  }
   c->epoch += 1;
   const uint32_t epoch = c->epoch;
   const int64_t out_area = batch * sl * heads_total * Dh * 2;

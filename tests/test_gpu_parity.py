@@ -787,3 +787,32 @@ def test_ulysses_attention_full_cfg5_vs_sdpa():
             got = out[r, 0][rows][:, grp * hl * Dh:(grp + 1) * hl * Dh].view(-1, hl, Dh).permute(1, 0, 2)
             err = (got.float() - ref.float()).abs().max().item()
             assert err <= 2e-2 * ref.float().abs().max().item() + 2e-3, (r, grp, err)
+
+
+def test_cuda_graph_capture_policy():
+    """Single-rank calls capture into a CUDA graph and replay correctly; multi-rank fused
+    collectives refuse capture loudly (their per-call epochs are host-side)."""
+    g = torch.Generator(device=DEV).manual_seed(4)
+    a = torch.randn((512, 256), device=DEV, generator=g).to(torch.bfloat16)
+    b = torch.randn((256, 384), device=DEV, generator=g).to(torch.bfloat16)
+    c = torch.empty((512, 384), device=DEV)
+    s = torch.cuda.Stream(DEV)
+    tpf.gemm(a, b, c, stream=s)  # warm-up outside capture (first-call attribute setup)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        tpf.gemm(a, b, c, stream=s)
+    c.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.allclose(c, a.float() @ b.float(), rtol=1e-3, atol=1e-2)
+
+    comm = tpf.Communicator.local_group(2, tpf.sym_bytes_rs(2, 1, 256, 128, 256, 1))
+    x = torch.zeros((2, 1, 256, 128), device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros((2, 128, 256), device=DEV, dtype=torch.bfloat16)
+    y = torch.zeros((2, 1, 128, 256), device=DEV)
+    graph2 = torch.cuda.CUDAGraph()
+    with pytest.raises(ValueError, match="CUDA graph"):
+        with torch.cuda.graph(graph2, stream=s):
+            comm.gemm_rs(x, w, y, stream=s)
+    comm.close()
