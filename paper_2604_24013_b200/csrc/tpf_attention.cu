@@ -137,10 +137,14 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   const int per_step = p.G * npair;
   const int nitems = p.T * per_step;
 
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = p.epoch_dev ? epoch_read(p.epoch_dev, p.epoch_bump) : p.epoch;
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&p.tmap_q);
-    prefetch_tmap(&p.tmap_k);
-    prefetch_tmap(&p.tmap_v);
+    for (int par = 0; par < 2; ++par) {
+      prefetch_tmap(&p.tmap_q[par]);
+      prefetch_tmap(&p.tmap_k[par]);
+      prefetch_tmap(&p.tmap_v[par]);
+    }
   }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
@@ -161,6 +165,11 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;  // S0 @ 0, S1 @ 128, O0 @ 256, O1 @ 384
+  const uint32_t epoch = s_epoch;
+  const int par = p.epoch_dev ? static_cast<int>(epoch & 1u) : p.parity;
+  const CUtensorMap* tmq = &p.tmap_q[par];
+  const CUtensorMap* tmk = &p.tmap_k[par];
+  const CUtensorMap* tmv = &p.tmap_v[par];
   // Register split: warps 0-3 (TMA, MMA, TMEM) need few, the softmax warpgroups hold a whole
   // 128-wide S row: 72 * 128 + 216 * 256 = 168 * 384, exactly the pool the CTA launched with.
   // setmaxnreg.inc blocks until the pool can satisfy it, so the sum must not exceed the pool
@@ -182,8 +191,8 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         mbar_arrive_expect_tx(q_full, 2 * kFTileBytes);
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
-          tma_load_4d(sq + w * kFTileBytes, &p.tmap_q, q_full, 0, row0 + w * kFTile, g, h);
-          tma_load_4d(sq + w * kFTileBytes + kFAtom, &p.tmap_q, q_full, 64, row0 + w * kFTile, g, h);
+          tma_load_4d(sq + w * kFTileBytes, tmq, q_full, 0, row0 + w * kFTile, g, h);
+          tma_load_4d(sq + w * kFTileBytes + kFAtom, tmq, q_full, 64, row0 + w * kFTile, g, h);
         }
         for (int j = 0; j < p.nkv; ++j) {
 #pragma unroll
@@ -191,7 +200,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
             const int slot = rc % kFRing;
             fmha_wait(p, r_empty + slot, ((rc / kFRing) & 1) ^ 1);
             uint8_t* dst = ring + slot * kFTileBytes;
-            const CUtensorMap* tm = kv ? &p.tmap_v : &p.tmap_k;
+            const CUtensorMap* tm = kv ? tmv : tmk;
             mbar_arrive_expect_tx(r_full + slot, kFTileBytes);
             tma_load_4d(dst, tm, r_full + slot, 0, j * kFTile, g, h);
             tma_load_4d(dst + kFAtom, tm, r_full + slot, 64, j * kFTile, g, h);
@@ -378,7 +387,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       if (qt < p.nqt) {
         const float inv = 1.f / lsum;
         const int b = g / p.heads, hh = g - b * p.heads;
-        char* orow = p.recv[dst] +
+        char* orow = p.recv[par][dst] +
                      ((static_cast<int64_t>(b) * p.sl + qt * kFTile + row) * p.fw +
                       (static_cast<int64_t>(p.local ? 0 : rank) * p.heads + hh) * kFTile) * 2;
 #pragma unroll
@@ -400,9 +409,9 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
           fence_sys();
           __syncwarp();
           if (lane == 0 && rank != p.fault_rank)
-            st_relaxed_sys(p.flags[dst] + static_cast<int64_t>(rank) * p.nflags_per_src +
+            st_relaxed_sys(p.flags[par][dst] + static_cast<int64_t>(rank) * p.nflags_per_src +
                                (static_cast<int64_t>(g) * p.nqt + qt) * 4 + ew,
-                           p.epoch);
+                           epoch);
         }
       }
       // O_w is read (tcgen05.ld waited) before this warp's next p_ready arrival, and PV_w(0)
@@ -415,6 +424,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem);
+  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, epoch);
 }
 
 cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream) {

@@ -112,7 +112,58 @@ __global__ void wait_flags_kernel(const uint32_t* flags, int64_t n, uint32_t epo
   }
 }
 
+__global__ void wait_flags2_kernel(const uint32_t* flags0, const uint32_t* flags1, int64_t n,
+                                   const uint32_t* epoch_dev, uint32_t epoch_static, int64_t timeout_ns,
+                                   uint32_t* err, int rank) {
+  const uint32_t epoch = epoch_dev ? epoch_read(epoch_dev, 0) : epoch_static;
+  const uint32_t* flags = (epoch_dev && (epoch & 1u)) ? flags1 : flags0;
+  const uint64_t t0 = globaltimer();
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    while (ld_relaxed_sys(flags + i) < epoch) {
+      if (ld_relaxed_sys(err + 4)) return;
+      if (globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
+        if (atomicCAS(err, 0u, 1u) == 0u) {
+          err[1] = static_cast<uint32_t>(rank);
+          err[2] = 0xFFFFFFFFu;
+          err[3] = static_cast<uint32_t>(i);
+        }
+        atomicExch(err + 4, 1u);
+        return;
+      }
+      __nanosleep(64);
+    }
+    (void)ld_acquire_sys(flags + i);
+  }
+}
+
+__global__ void copy_by_parity_kernel(int4* dst, const int4* src0, const int4* src1, int64_t n,
+                                      const uint32_t* epoch_dev) {
+  const int4* src = (epoch_read(epoch_dev, 0) & 1u) ? src1 : src0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[i] = src[i];
+}
+
 }  // namespace
+
+void launch_wait_flags2(const uint32_t* flags0, const uint32_t* flags1, int64_t n, const uint32_t* epoch_dev,
+                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, cudaStream_t st) {
+  if (n <= 0) return;
+  const int threads = 256;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 64));
+  wait_flags2_kernel<<<blocks, threads, 0, st>>>(flags0, flags1, n, epoch_dev, epoch, timeout_ns, err, rank);
+}
+
+void launch_copy_by_parity(void* dst, const void* src0, const void* src1, int64_t bytes, const uint32_t* epoch_dev,
+                           cudaStream_t st) {
+  const int64_t n = bytes / 16;
+  if (n <= 0) return;
+  const int threads = 512;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 4 * 148));
+  copy_by_parity_kernel<<<blocks, threads, 0, st>>>(static_cast<int4*>(dst), static_cast<const int4*>(src0),
+                                                    static_cast<const int4*>(src1), n, epoch_dev);
+}
 
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st) {
   softmax_rows_kernel<<<static_cast<unsigned>(rows), 256, 0, st>>>(s, static_cast<__nv_bfloat16*>(p), cols,

@@ -38,7 +38,7 @@ constexpr int kErrWords = 8;
 struct KParams {
   CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); a_mn: (rows, K, B, ranks)
   CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); b_kmajor: (K, N, ranks)
-  CUtensorMap tmap_wire;  // AG wire images (128 B, 128 rows, image, slot, hosted rank), no swizzle
+  CUtensorMap tmap_wire[2];  // AG wire images per heap parity (128 B, 128 rows, image, slot, rank)
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
   int mode;            // Mode (kernel instance)
   int T;               // group size
@@ -84,8 +84,10 @@ struct KParams {
   int64_t flag_off[2];      // per parity: flag region offset
   int64_t slot_bytes;       // one slot (one (pass, iteration) message)
   int64_t flags_per_slot;
-  uint32_t epoch;
+  uint32_t epoch;      // static epoch / parity, used when epoch_dev is null (T == 1 calls)
   int parity;
+  uint32_t* epoch_dev; // device epoch [value, exit counter]: read at entry (+ epoch_bump), and
+  int epoch_bump;      // the last CTA to exit publishes the value (CUDA-graph replayable)
   int8_t sched[kMaxRanks][kMaxRanks][3];  // [rank][step] (send, recv, slice)
   uint32_t* err;
   int64_t timeout_ns;
@@ -109,15 +111,19 @@ enum TraceKind : int {
 
 // UP v2: fused flash-attention + output all-to-all (csrc/tpf_attention.cu)
 struct FmhaParams {
-  CUtensorMap tmap_q, tmap_k, tmap_v;  // (Dh = 128, S, G, hosted ranks), box (64, 128), SW128
+  CUtensorMap tmap_q[2], tmap_k[2], tmap_v[2];  // per heap parity (a symmetric inbox differs per
+                                                // parity; user buffers: both the same)
   int T, R, rank0, heads, G, nqt, nkv, ctas_per_rank;
   int local;                           // 1: plain attention into recv[rank] (no all-to-all)
   int64_t S, sl, fw;                   // fw = T * heads * Dh (output row stride, elements)
   float scale_log2;                    // softmax scale * log2(e)
-  char* recv[kMaxRanks];               // every rank's receive buffer (peer-mapped)
-  uint32_t* flags[kMaxRanks];          // every rank's flag block (peer-mapped)
+  char* recv[2][kMaxRanks];            // [parity] every rank's receive buffer (peer-mapped)
+  uint32_t* flags[2][kMaxRanks];       // [parity] every rank's flag block (peer-mapped)
   int64_t nflags_per_src;              // G * nqt * 4
-  uint32_t epoch;
+  uint32_t epoch;                      // static epoch / parity when epoch_dev is null
+  int parity;
+  uint32_t* epoch_dev;                 // device epoch (see KParams)
+  int epoch_bump;
   int fault_rank;
   uint32_t* err;
   int64_t timeout_ns;
@@ -127,12 +133,12 @@ struct FmhaParams {
 struct UlyssesParams {
   const char* src[3];               // q, k, v of hosted rank 0: (B*H, sl, Dh) bf16
   int64_t src_rank_stride;          // bytes between hosted ranks' inputs
-  char* dst[kMaxRanks];             // every rank's inbox: [q | k | v], each (B*hl, S, Dh)
-  uint32_t* flags[kMaxRanks];       // every rank's a2a flag block: [src rank][cta]
+  char* dst[2][kMaxRanks];          // [parity] every rank's inbox: [q | k | v], each (B*hl, S, Dh)
+  uint32_t* flags[2][kMaxRanks];    // [parity] every rank's a2a flag block: [src rank][cta]
   int64_t tensor_bytes;             // B*hl*S*Dh*2
   int64_t B, H, hl, S, sl, Dh;
   int T, R, rank0, ctas_per_rank;
-  uint32_t epoch;
+  uint32_t* epoch_dev;              // device epoch: this launch opens the call (bump)
   int fault_rank;
 };
 
@@ -140,6 +146,13 @@ void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream);
 void launch_fused(const KParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
+// Wait until flags[parity][0..n) >= epoch, epoch / parity read from epoch_dev (the call's
+// current device epoch), or the given static epoch / flags[0] when epoch_dev is null.
+void launch_wait_flags2(const uint32_t* flags0, const uint32_t* flags1, int64_t n, const uint32_t* epoch_dev,
+                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, cudaStream_t st);
+// dst <- src[parity of the call's device epoch], `bytes` a multiple of 16.
+void launch_copy_by_parity(void* dst, const void* src0, const void* src1, int64_t bytes, const uint32_t* epoch_dev,
+                           cudaStream_t st);
 void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
                        int rank, cudaStream_t st);
 int max_pairs();

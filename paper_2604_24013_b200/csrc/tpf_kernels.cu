@@ -38,6 +38,10 @@ namespace tpf {
 
 namespace {
 
+// This launch's epoch / heap parity (from the device epoch when the call is multi-rank).
+__shared__ uint32_t s_epoch;
+__shared__ int s_parity;
+
 struct Tile {
   int step, mb, nt, b, row0, valid;  // mb: THIS CTA's m-block; valid rows (0: dummy CTA)
   int pair;                          // m-block pair index within the step
@@ -102,8 +106,8 @@ __device__ __noinline__ void record_error(const KParams& p, uint32_t code, int r
 // semantics; on timeout / abort returns false (the kernel then drains with garbage
 // and the host raises from the error record).
 __device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, int rank,
-                                          int step, int tile) {
-  if (ld_relaxed_sys(f) >= p.epoch) {
+                                          int step, int tile, uint32_t epoch) {
+  if (ld_relaxed_sys(f) >= epoch) {
     (void)ld_acquire_sys(f);
     return true;
   }
@@ -111,7 +115,7 @@ __device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, i
   while (true) {
 #pragma unroll 1
     for (int k = 0; k < 256; ++k) {
-      if (ld_relaxed_sys(f) >= p.epoch) {
+      if (ld_relaxed_sys(f) >= epoch) {
         (void)ld_acquire_sys(f);
         return true;
       }
@@ -136,13 +140,13 @@ __device__ __forceinline__ void mbar_wait(const KParams& p, uint64_t* bar, uint3
   }
 }
 
-__device__ __forceinline__ char* slot_ptr(const KParams& p, int rank, int slot) {
-  return p.sym[rank] + p.data_off[p.parity] + static_cast<int64_t>(slot) * p.slot_bytes;
+__device__ __forceinline__ char* slot_ptr(const KParams& p, int par, int rank, int slot) {
+  return p.sym[rank] + p.data_off[par] + static_cast<int64_t>(slot) * p.slot_bytes;
 }
 
-__device__ __forceinline__ uint32_t* flag_ptr(const KParams& p, int rank, int slot,
+__device__ __forceinline__ uint32_t* flag_ptr(const KParams& p, int par, int rank, int slot,
                                               int64_t idx) {
-  return reinterpret_cast<uint32_t*>(p.sym[rank] + p.flag_off[p.parity]) +
+  return reinterpret_cast<uint32_t*>(p.sym[rank] + p.flag_off[par]) +
          static_cast<int64_t>(slot) * p.flags_per_slot + idx;
 }
 
@@ -317,7 +321,15 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tmap_a);
     prefetch_tmap(&p.tmap_b);
-    if (kOp == OP_AG && p.T > 1) prefetch_tmap(&p.tmap_wire);
+    if (kOp == OP_AG && p.T > 1) {
+      prefetch_tmap(&p.tmap_wire[0]);
+      prefetch_tmap(&p.tmap_wire[1]);
+    }
+  }
+  if (threadIdx.x == 0) {
+    const uint32_t e = p.epoch_dev ? epoch_read(p.epoch_dev, p.epoch_bump) : p.epoch;
+    s_epoch = e;
+    s_parity = p.epoch_dev ? static_cast<int>(e & 1u) : p.parity;
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -337,6 +349,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const uint32_t ep = s_epoch;  // this launch's epoch / heap parity, in registers from here on
+  const int par = s_parity;
+  const CUtensorMap* wmap = &p.tmap_wire[par];
 
   if (!active) {
   } else if (warp == 0) {
@@ -367,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
                                       : static_cast<int64_t>(t.mb) * p.nkb;
       const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
-      const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, rank, aslot, img0) : nullptr;
+      const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
       int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
       uint64_t t_first = 0;
       const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
@@ -378,12 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           // acquire-loads one flag (system scope), the warp barrier carries that ordering to
           // lane 0, whose proxy fence orders it before the TMA (async-proxy) reads.
           const uint64_t tw0 = p.trace ? globaltimer() : 0;
-          if (lane == 0) wait_flag(p, mflags + kb, rank, t.step, lin);
+          if (lane == 0) wait_flag(p, mflags + kb, rank, t.step, lin, ep);
           __syncwarp();
           ready = kb;
           while (ready + 1 < p.nkb) {
             const int k = ready + 1 + lane;
-            const bool ok = k >= p.nkb || ld_acquire_sys(mflags + k) >= p.epoch;
+            const bool ok = k >= p.nkb || ld_acquire_sys(mflags + k) >= ep;
             const uint32_t m = __ballot_sync(0xffffffffu, ok);
             const int run = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
             ready = min(ready + run, p.nkb - 1);
@@ -409,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           else
             mbar_arrive_cluster(fb);
           if (a_from_wire) {
-            tma_load_2sm_5d(sa, &p.tmap_wire, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
+            tma_load_2sm_5d(sa, wmap, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
           } else if (kAMn) {
             // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
 #pragma unroll
@@ -420,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
           }
           if (b_from_wire) {
-            tma_load_2sm_5d(sb, &p.tmap_wire, fb, 0, 0, img, aslot, h);
+            tma_load_2sm_5d(sb, wmap, fb, 0, 0, img, aslot, h);
           } else if (kBKMajor) {
             // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
             if (kBBatched)
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         fence_sys();
         __syncwarp();
         if (lane == 0 && rank != p.fault_rank)
-          for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], p.epoch);
+          for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], ep);
         if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
         nunpub = 0;
       };
@@ -545,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           if (live) {
             const int64_t img = img0 + kb;
             const uint4* src = reinterpret_cast<const uint4*>(sbase + stage * kAStageBytes);
-            uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, dst_rank, slot) + img * kAStageBytes);
+            uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes);
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
               uint4 v[16];
@@ -554,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 #pragma unroll
               for (int i = 0; i < 16; ++i) dst[(half * 16 + i) * 32 + lane] = v[i];
             }
-            unpub[nunpub++] = flag_ptr(p, dst_rank, slot, img);
+            unpub[nunpub++] = flag_ptr(p, par, dst_rank, slot, img);
           }
           __syncwarp();  // every lane's SMEM reads of the stage are done
           if (lane == 0) mbar_arrive(empty + stage);
@@ -584,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       fence_sys();
       __syncwarp();
       if (lane == 0 && rank != p.fault_rank)
-        for (int i = 0; i < npend; ++i) st_relaxed_sys(pend[i], p.epoch);
+        for (int i = 0; i < npend; ++i) st_relaxed_sys(pend[i], ep);
       npend = 0;
     };
     int lt = 0;
@@ -655,23 +670,23 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       if (tile_live && !p.direct && it > 0 && !p.compute_only) {
         const int slot_in = slot_send - 1;
         const uint64_t tw0 = (p.trace && lane == 0) ? globaltimer() : 0;
-        const uint32_t* fin = flag_ptr(p, rank, slot_in, fidx);
-        if (npend > 0 && ld_relaxed_sys(fin) < p.epoch) publish();
-        wait_flag(p, fin, rank, t.step, lin);
+        const uint32_t* fin = flag_ptr(p, par, rank, slot_in, fidx);
+        if (npend > 0 && ld_relaxed_sys(fin) < ep) publish();
+        wait_flag(p, fin, rank, t.step, lin, ep);
         if (p.trace && lane == 0 && ew == 0) {
           const uint64_t tw1 = globaltimer();
           if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_IN, rank, t.step, lin, tw0, tw1);
         }
-        inbox = slot_ptr(p, rank, slot_in) + tile_idx * tile_bytes;
+        inbox = slot_ptr(p, par, rank, slot_in) + tile_idx * tile_bytes;
       }
       if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
         publish();
         for (int s = 0; s < p.T - 1; ++s)
-          wait_flag(p, flag_ptr(p, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin);
+          wait_flag(p, flag_ptr(p, par, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin, ep);
       }
       __syncwarp();
       char* dst_tile =
-          (last || !tile_live) ? nullptr : slot_ptr(p, send_rank, slot_send) + tile_idx * tile_bytes;
+          (last || !tile_live) ? nullptr : slot_ptr(p, par, send_rank, slot_send) + tile_idx * tile_bytes;
       // heads_merge (UP): batch g = b*heads + hh -> rows of b, columns hh*N (merge_heads fused)
       const int hm = kUpEpi ? p.heads_merge : 0;
       const int64_t ob = hm ? t.b / hm : t.b;
@@ -695,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
           } else if (p.direct && last && p.T > 1 && !p.compute_only) {
             // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
-            const char* in0 = slot_ptr(p, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
+            const char* in0 = slot_ptr(p, par, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
             direct_fold(p, in0, j, row, v);
           }
           if (last)
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
       if (!last && tile_live) {
-        pend[npend++] = flag_ptr(p, send_rank, slot_send, fidx);
+        pend[npend++] = flag_ptr(p, par, send_rank, slot_send, fidx);
         if (npend == kPend) publish();
         if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_FLAG, rank, t.step, lin, t_epi0, globaltimer());
       }
@@ -716,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         // completion flag for a pushed output tile (UP all-to-all)
         fence_sys();
         __syncwarp();
-        if (lane == 0 && rank != p.fault_rank) st_relaxed_sys(p.done_rank[h] + fidx, p.epoch);
+        if (lane == 0 && rank != p.fault_rank) st_relaxed_sys(p.done_rank[h] + fidx, ep);
       }
       if (p.trace && lane == 0 && ew == 0 && tile_live)
         trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());
@@ -728,6 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_2sm<512>(tmem_base);
+  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, ep);
 }
 
 namespace {

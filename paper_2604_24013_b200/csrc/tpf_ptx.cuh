@@ -114,6 +114,25 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       : "memory");
 }
 
+// ---------------------------------------------------------------- device epochs
+// A multi-rank call's epoch lives in device memory so that CUDA-graph replays advance it:
+// every CTA reads it at entry (plus one for the launch that opens a call), and the last CTA
+// of that launch to exit publishes the new value for the next stream-ordered launch.
+__device__ __forceinline__ uint32_t epoch_read(const uint32_t* ep, int bump) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(ep));
+  return v + (bump ? 1u : 0u);
+}
+__device__ __forceinline__ void epoch_publish(uint32_t* ep, uint32_t value) {
+  // one thread per CTA, after the CTA's last use of the epoch
+  __threadfence();
+  if (atomicAdd(ep + 1, 1u) == gridDim.x - 1) {
+    ep[1] = 0;
+    ep[0] = value;
+    __threadfence();
+  }
+}
+
 // Warp-wide variants: every lane executes the call with the same (warp-uniform) operands and
 // elect.sync picks the issuing lane inside the asm. Keeping the whole warp converged lets ptxas
 // hold descriptors in uniform registers instead of re-broadcasting them per instruction, which

@@ -140,7 +140,8 @@ struct tpf_comm {
   char* sym[tpf::kMaxRanks] = {};
   bool opened[tpf::kMaxRanks] = {};
   bool peers_ready = false;
-  uint32_t epoch = 0;
+  uint32_t epoch = 0;           // host mirror, used only by the unfused attention fallback
+  uint32_t* dev_epoch = nullptr;  // device epoch [value, exit counter] (graph-replayable calls)
   uint32_t* err = nullptr;      // device error record
   int64_t timeout_ns = kDefaultTimeoutNs;
   int device = 0;
@@ -342,33 +343,38 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
     p.flag_off[1] = kFlagBytesPerParity;
     p.data_off[0] = 2 * kFlagBytesPerParity;
     p.data_off[1] = 2 * kFlagBytesPerParity + data_cap;
-    p.parity = static_cast<int>((c->epoch + 1) & 1u);
     p.slot_bytes = slot_bytes;
     p.flags_per_slot = flags_per_slot;
     if (k.op == tpf::OP_AG) {
-      // AG wire images of the hosted ranks' local slots: (128 B, 128 rows, image, slot, rank)
+      // AG wire images of the hosted ranks' local slots: (128 B, 128 rows, image, slot, rank),
+      // one map per heap parity (the kernel picks by the device epoch)
       const int64_t rank_stride = R > 1 ? static_cast<int64_t>(c->sym_bytes) : nslots * slot_bytes;
       const uint64_t dims[5] = {64, tpf::BM, static_cast<uint64_t>(flags_per_slot),
                                 static_cast<uint64_t>(nslots), static_cast<uint64_t>(R)};
       const uint64_t strides[4] = {128, tpf::kAStageBytes, static_cast<uint64_t>(slot_bytes),
                                    static_cast<uint64_t>(rank_stride)};
       const uint32_t box[5] = {64, tpf::BM, 1, 1, 1};
-      tpf::Status s = make_tmap(&p.tmap_wire, c->sym[k.rank0] + p.data_off[p.parity], 5, dims,
-                                strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
-      if (!s.good()) return s;
+      for (int par = 0; par < 2; ++par) {
+        tpf::Status s = make_tmap(&p.tmap_wire[par], c->sym[k.rank0] + p.data_off[par], 5, dims, strides, box,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (!s.good()) return s;
+      }
     }
-    {
-      const tpf::Status cs = check_not_capturing(c, stream);
-      if (!cs.good()) return cs;
-    }
-    c->epoch += 1;
-    p.epoch = c->epoch;
-    p.parity = static_cast<int>(c->epoch & 1u);
+    // epoch: in device memory, advanced by the launch that opens the call
+    p.epoch_dev = c->dev_epoch;
+    p.epoch_bump = k.no_epoch ? 0 : 1;
+    p.epoch = 0;
+    p.parity = 0;
   } else {
     p.sched[0][0][0] = -1;
     p.sched[0][0][1] = -1;
     p.sched[0][0][2] = 0;
-    p.epoch = (c && k.no_epoch) ? c->epoch : 1;
+    // single-rank step: no ring flags; a step of a multi-launch collective (UP fallback)
+    // publishes done flags with the call's current device epoch
+    p.epoch_dev = (c && k.no_epoch) ? c->dev_epoch : nullptr;
+    p.epoch_bump = 0;
+    p.epoch = 1;
+    p.parity = 0;
   }
   p.err = c ? c->err : default_err_buffer();
   if (!p.err) return tpf::Status::cuda("no device error buffer (CUDA unavailable)");
@@ -454,9 +460,13 @@ int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out) {
   if (e == cudaSuccess) e = cudaMemset(c->local, 0, sym_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
+    if (c->err) cudaFree(c->err);
+    if (c->dev_epoch) cudaFree(c->dev_epoch);
     delete c;
     return fail(tpf::Status::cuda(std::string("tpf_comm_create: ") + cudaGetErrorString(e)));
   }
@@ -508,9 +518,13 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
   if (e == cudaSuccess) e = cudaMemset(c->local, 0, per * world);
   if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
+    if (c->err) cudaFree(c->err);
+    if (c->dev_epoch) cudaFree(c->dev_epoch);
     delete c;
     return fail(tpf::Status::cuda(std::string("tpf_comm_create_local_group: ") + cudaGetErrorString(e)));
   }
@@ -527,6 +541,7 @@ int tpf_comm_destroy(tpf_comm* c) {
     if (c->opened[r]) cudaIpcCloseMemHandle(c->sym[r]);
   if (c->local) cudaFree(c->local);
   if (c->err) cudaFree(c->err);
+  if (c->dev_epoch) cudaFree(c->dev_epoch);
   if (c->scratch) cudaFree(c->scratch);
   delete c;
   return TPF_OK;
@@ -679,9 +694,11 @@ int tpf_dp_param_ag_gemm(tpf_comm* c, const void* x, const void* w_rows, void* o
 }
 
 // Fused flash attention + output all-to-all (UP v2, Dh = 128). q/k/v: (G, S, 128) bf16 per hosted
-// rank, hosted ranks `rstride` bytes apart. Uses (and does not bump) `epoch`.
-static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* q, const void* k, const void* v, uint64_t rstride,
-                               void* out, int64_t batch, int64_t heads, int64_t S, uint32_t epoch, int scale,
+// rank, hosted ranks `rstride` bytes apart; qkv1 (may equal qkv) are the inputs to use when the
+// call's heap parity is 1 (a symmetric inbox). `bump`: this launch opens the call (advances the
+// device epoch); otherwise an earlier launch of the call did.
+static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* const qkv[3], const void* const qkv1[3], uint64_t rstride,
+                               void* out, int64_t batch, int64_t heads, int64_t S, int bump, int scale,
                                cudaStream_t stream) {
   const int T = c->world;
   const int R = hosted(c);
@@ -691,31 +708,38 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* q, const void* k, const 
   const int64_t nflags2 = G * (sl / 128) * 4;
   if (nflags2 * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
     return tpf::Status::capacity("symmetric heap too small for the attention all-to-all");
-  const int par = static_cast<int>(epoch & 1u);
-  auto recv_at = [&](int rank) {
+  auto recv_at = [&](int rank, int par) {
     return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes);
   };
-  auto flags_at = [&](int rank) { return reinterpret_cast<uint32_t*>(c->sym[rank] + par * kFlagBytesPerParity); };
+  auto flags_at = [&](int rank, int par) {
+    return reinterpret_cast<uint32_t*>(c->sym[rank] + par * kFlagBytesPerParity);
+  };
   tpf::FmhaParams fp;
   std::memset(&fp, 0, sizeof(fp));
   const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
                             static_cast<uint64_t>(R)};
   const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2), rstride};
   const uint32_t box[4] = {64, 128, 1, 1};
-  tpf::Status s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
-  if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
-  if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
+  tpf::Status s;
+  for (int par = 0; par < 2 && s.good(); ++par) {
+    const void* const* in = par ? qkv1 : qkv;
+    s = make_tmap(&fp.tmap_q[par], in[0], 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_k[par], in[1], 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_v[par], in[2], 4, dims, strides, box);
+  }
   if (!s.good()) return s;
   fp.T = T; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
   fp.nqt = static_cast<int>(sl / 128); fp.nkv = static_cast<int>(S / 128);
   fp.S = S; fp.sl = sl; fp.fw = fw;
   fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
-  for (int x = 0; x < T; ++x) {
-    fp.recv[x] = recv_at(x);
-    fp.flags[x] = flags_at(x);
-  }
+  for (int par = 0; par < 2; ++par)
+    for (int x = 0; x < T; ++x) {
+      fp.recv[par][x] = recv_at(x, par);
+      fp.flags[par][x] = flags_at(x, par);
+    }
   fp.nflags_per_src = nflags2;
-  fp.epoch = epoch;
+  fp.epoch_dev = c->dev_epoch;
+  fp.epoch_bump = bump;
   fp.fault_rank = c->fault_rank;
   fp.err = c->err;
   fp.timeout_ns = c->timeout_ns;
@@ -724,12 +748,15 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* q, const void* k, const 
   TPF_CUDA_TRY_STATUS(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
   for (int hh = 0; hh < R; ++hh) {
     const int rank = r0 + hh;
-    uint32_t* f = flags_at(rank);
-    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags2, epoch, c->timeout_ns, c->err, rank, stream);
-    tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags2, static_cast<int64_t>(T - 1 - rank) * nflags2,
-                           epoch, c->timeout_ns, c->err, rank, stream);
-    TPF_CUDA_TRY_STATUS(cudaMemcpyAsync(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank), recv_bytes,
-                                        cudaMemcpyDeviceToDevice, stream));
+    uint32_t* f0 = flags_at(rank, 0);
+    uint32_t* f1 = flags_at(rank, 1);
+    tpf::launch_wait_flags2(f0, f1, static_cast<int64_t>(rank) * nflags2, c->dev_epoch, 0, c->timeout_ns, c->err,
+                            rank, stream);
+    const int64_t off = static_cast<int64_t>(rank + 1) * nflags2;
+    tpf::launch_wait_flags2(f0 + off, f1 + off, static_cast<int64_t>(T - 1 - rank) * nflags2, c->dev_epoch, 0,
+                            c->timeout_ns, c->err, rank, stream);
+    tpf::launch_copy_by_parity(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank, 0), recv_at(rank, 1),
+                               recv_bytes, c->dev_epoch, stream);
   }
   TPF_CUDA_TRY_STATUS(cudaGetLastError());
   return tpf::Status::ok();
@@ -764,16 +791,17 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   };
   if (Dh == 128 && sl % 128 == 0) {
     // v2: one persistent fused flash-attention launch for all steps / heads / hosted ranks
-    {
-    const tpf::Status cs = check_not_capturing(c, stream);
-    if (!cs.good()) return fail(cs);
-  }
-  c->epoch += 1;
-    s = fmha_a2a_v2(c, q, k, v, static_cast<uint64_t>(G * S * Dh * 2), out, batch, heads, S, c->epoch, scale,
+    const void* qkv[3] = {q, k, v};
+    s = fmha_a2a_v2(c, qkv, qkv, static_cast<uint64_t>(G * S * Dh * 2), out, batch, heads, S, /*bump=*/1, scale,
                     stream);
     return s.good() ? TPF_OK : fail(s);
   }
-  // v1 (any head_dim): scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S)
+  // v1 (any head_dim): scores fp32 (R, G, sl, S), probabilities bf16 (R, G, sl, S).
+  // Not graph-capturable (host-side epoch read, scratch allocation): refuse before any work.
+  {
+    const tpf::Status cs = check_not_capturing(c, stream);
+    if (!cs.good()) return fail(cs);
+  }
   const size_t sc_bytes = static_cast<size_t>(R) * G * sl * S * 4, pb_bytes = sc_bytes / 2;
   if (c->scratch_bytes < sc_bytes + pb_bytes) {
     if (c->scratch) cudaFree(c->scratch);
@@ -784,12 +812,13 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   }
   float* scores = reinterpret_cast<float*>(c->scratch);
   char* probs = c->scratch + sc_bytes;
-  {
-    const tpf::Status cs = check_not_capturing(c, stream);
-    if (!cs.good()) return fail(cs);
-  }
-  c->epoch += 1;
-  const uint32_t epoch = c->epoch;
+  // This multi-launch fallback computes parity-specific pointers on the host, so it opens
+  // the call by reading and advancing the device epoch synchronously (not graph-capturable).
+  uint32_t epoch = 0;
+  TPF_CUDA_TRY(cudaStreamSynchronize(stream));
+  TPF_CUDA_TRY(cudaMemcpy(&epoch, c->dev_epoch, sizeof(epoch), cudaMemcpyDeviceToHost));
+  epoch += 1;
+  TPF_CUDA_TRY(cudaMemcpy(c->dev_epoch, &epoch, sizeof(epoch), cudaMemcpyHostToDevice));
   const int par = static_cast<int>(epoch & 1u);
   auto recv_of = [&](int rank) { return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes); };
   auto flags_of = [&](int rank) {
@@ -877,15 +906,19 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   const uint64_t strides[3] = {static_cast<uint64_t>(Dh * 2), static_cast<uint64_t>(S * Dh * 2),
                                static_cast<uint64_t>(G * S * Dh * 2)};
   const uint32_t box[4] = {64, 128, 1, 1};
-  s = make_tmap(&fp.tmap_q, q, 4, dims, strides, box);
-  if (s.good()) s = make_tmap(&fp.tmap_k, k, 4, dims, strides, box);
-  if (s.good()) s = make_tmap(&fp.tmap_v, v, 4, dims, strides, box);
+  for (int par = 0; par < 2 && s.good(); ++par) {  // user buffers: both parities the same
+    s = make_tmap(&fp.tmap_q[par], q, 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_k[par], k, 4, dims, strides, box);
+    if (s.good()) s = make_tmap(&fp.tmap_v[par], v, 4, dims, strides, box);
+  }
   if (!s.good()) return fail(s);
   fp.T = 1; fp.local = 1; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
   fp.nqt = static_cast<int>(S / 128); fp.nkv = static_cast<int>(S / 128);
   fp.S = S; fp.sl = S; fp.fw = hd;
   fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
-  for (int hh = 0; hh < R; ++hh) fp.recv[r0 + hh] = c->scratch + static_cast<size_t>(hh) * batch * S * hd * 2;
+  for (int hh = 0; hh < R; ++hh)
+    fp.recv[0][r0 + hh] = fp.recv[1][r0 + hh] = c->scratch + static_cast<size_t>(hh) * batch * S * hd * 2;
+  fp.epoch_dev = nullptr;  // local attention: no flags; the GEMM-RS below opens the call
   fp.err = c->err;
   fp.timeout_ns = c->timeout_ns;
   fp.fault_rank = -1;
@@ -1015,16 +1048,16 @@ int tpf_gemm_rs(tpf_comm* c, const void* x, const void* w, void* out, int64_t B,
 // all-to-all (fuse_all_to_all_attention). Inbox layout per parity, after the attention's
 // output area: [q | k | v], each (batch*heads_local, S, Dh) bf16. The a2a flags sit after
 // the attention's flags in the same parity block: [source rank][cta].
+// Opens the call (the push kernel advances the device epoch). inbox_local[par] receives this
+// process's hosted rank 0 inbox for heap parity par.
 static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, const void* v, int64_t batch,
-                                     int64_t heads_total, int64_t S, int64_t Dh, uint32_t epoch,
-                                     int64_t out_area_bytes, int64_t flag_off, char** inbox_local,
-                                     cudaStream_t stream) {
+                                     int64_t heads_total, int64_t S, int64_t Dh, int64_t out_area_bytes,
+                                     int64_t flag_off, char* inbox_local[2], cudaStream_t stream) {
   const int T = c->world;
   const int R = hosted(c);
   const int r0 = c->local_group ? 0 : c->rank;
   const int64_t hl = heads_total / T, sl = S / T;
   const int64_t tensor_bytes = batch * hl * S * Dh * 2;
-  const int par = static_cast<int>(epoch & 1u);
   const int64_t inbox_off = (out_area_bytes + 4095) & ~int64_t{4095};
   if (inbox_off + 3 * tensor_bytes > data_bytes_per_parity(c->sym_bytes))
     return tpf::Status::capacity("symmetric heap too small for the Ulysses all-to-all (need " +
@@ -1042,20 +1075,22 @@ static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, 
   up.ctas_per_rank = std::max(1, std::min(tpf::num_sms() / R, 132));
   if ((flag_off + static_cast<int64_t>(T) * up.ctas_per_rank) * 4 > kFlagBytesPerParity)
     return tpf::Status::capacity("flag block too small for the Ulysses all-to-all");
-  for (int x = 0; x < T; ++x) {
-    up.dst[x] = c->sym[x] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes) + inbox_off;
-    up.flags[x] = reinterpret_cast<uint32_t*>(c->sym[x] + par * kFlagBytesPerParity) + flag_off;
-  }
-  up.epoch = epoch;
+  for (int par = 0; par < 2; ++par)
+    for (int x = 0; x < T; ++x) {
+      up.dst[par][x] = c->sym[x] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes) + inbox_off;
+      up.flags[par][x] = reinterpret_cast<uint32_t*>(c->sym[x] + par * kFlagBytesPerParity) + flag_off;
+    }
+  up.epoch_dev = c->dev_epoch;
   up.fault_rank = c->fault_rank;
   tpf::launch_ulysses_push(up, stream);
   TPF_CUDA_TRY_STATUS(cudaGetLastError());
   for (int hh = 0; hh < R; ++hh) {
     const int rank = r0 + hh;
-    tpf::launch_wait_flags(up.flags[rank], static_cast<int64_t>(T) * up.ctas_per_rank, epoch, c->timeout_ns, c->err,
-                           rank, stream);
+    tpf::launch_wait_flags2(up.flags[0][rank], up.flags[1][rank], static_cast<int64_t>(T) * up.ctas_per_rank,
+                            c->dev_epoch, 0, c->timeout_ns, c->err, rank, stream);
   }
-  *inbox_local = up.dst[r0];
+  inbox_local[0] = up.dst[0][r0];
+  inbox_local[1] = up.dst[1][r0];
   return tpf::Status::ok();
 }
 
@@ -1079,20 +1114,16 @@ int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, vo
   if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
   if (!s.good()) return fail(s);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  {
-    const tpf::Status cs = check_not_capturing(c, stream);
-    if (!cs.good()) return fail(cs);
-  }
-  c->epoch += 1;
-  char* inbox = nullptr;
-  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, c->epoch, 0, 0, &inbox, stream);
+  char* inbox[2] = {nullptr, nullptr};
+  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, 0, 0, inbox, stream);
   if (!s.good()) return fail(s);
   const int64_t tb = batch * (heads_total / c->world) * S * Dh * 2;
   void* outs[3] = {q_out, k_out, v_out};
   for (int hh = 0; hh < hosted(c); ++hh)
     for (int t = 0; t < 3; ++t)
-      TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(outs[t]) + hh * tb, inbox + hh * c->sym_bytes + t * tb, tb,
-                                   cudaMemcpyDeviceToDevice, stream));
+      tpf::launch_copy_by_parity(static_cast<char*>(outs[t]) + hh * tb, inbox[0] + hh * c->sym_bytes + t * tb,
+                                 inbox[1] + hh * c->sym_bytes + t * tb, tb, c->dev_epoch, stream);
+  TPF_CUDA_TRY(cudaGetLastError());
   return TPF_OK;
 }
 
@@ -1106,20 +1137,16 @@ int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void*
   if (Dh != 128 || sl % 128)
     return fail(tpf::Status::shape("tpf_ulysses_attention: the fused path needs head_dim 128 and S/T % 128 == 0"));
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  {
-    const tpf::Status cs = check_not_capturing(c, stream);
-    if (!cs.good()) return fail(cs);
-  }
-  c->epoch += 1;
-  const uint32_t epoch = c->epoch;
   const int64_t out_area = batch * sl * heads_total * Dh * 2;
   const int64_t attn_flags = batch * hl * (sl / 128) * 4 * T;
-  char* inbox = nullptr;
-  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, epoch, out_area, (attn_flags + 31) & ~int64_t{31},
-                        &inbox, stream);
+  char* inbox[2] = {nullptr, nullptr};
+  s = ulysses_first_a2a(c, q, k, v, batch, heads_total, S, Dh, out_area, (attn_flags + 31) & ~int64_t{31}, inbox,
+                        stream);
   if (!s.good()) return fail(s);
   const int64_t tb = batch * hl * S * Dh * 2;
-  s = fmha_a2a_v2(c, inbox, inbox + tb, inbox + 2 * tb, static_cast<uint64_t>(c->sym_bytes), out, batch, hl, S, epoch,
-                  scale, stream);
+  const void* qkv0[3] = {inbox[0], inbox[0] + tb, inbox[0] + 2 * tb};
+  const void* qkv1[3] = {inbox[1], inbox[1] + tb, inbox[1] + 2 * tb};
+  // the push kernel opened the call; the attention reads that epoch
+  s = fmha_a2a_v2(c, qkv0, qkv1, static_cast<uint64_t>(c->sym_bytes), out, batch, hl, S, /*bump=*/0, scale, stream);
   return s.good() ? TPF_OK : fail(s);
 }

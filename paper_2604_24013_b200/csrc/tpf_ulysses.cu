@@ -33,6 +33,12 @@ __global__ void __launch_bounds__(kPushThreads) ulysses_push_kernel(UlyssesParam
   const int64_t pieces_per_block = (block_bytes + kPieceBytes - 1) / kPieceBytes;
   const int64_t blocks_per_dst = 3 * p.B * p.hl;  // (tensor, b, hh) for one head group
   const int64_t total = static_cast<int64_t>(T) * blocks_per_dst * pieces_per_block;
+  // this launch opens the call: epoch = device epoch + 1, heap parity = epoch & 1
+  __shared__ uint32_t s_epoch;
+  if (threadIdx.x == 0) s_epoch = epoch_read(p.epoch_dev, 1);
+  __syncthreads();
+  const uint32_t epoch = s_epoch;
+  const int par = static_cast<int>(epoch & 1u);
   for (int64_t w = cta; w < total; w += p.ctas_per_rank) {
     const int64_t piece = w % pieces_per_block;
     int64_t rest = w / pieces_per_block;
@@ -44,7 +50,7 @@ __global__ void __launch_bounds__(kPushThreads) ulysses_push_kernel(UlyssesParam
     const int g = static_cast<int>((rank + 1 + rest / 3) % T);  // rotated destination
     const char* src = p.src[tensor] + hosted * p.src_rank_stride +
                       ((b * p.H + g * p.hl + hh) * p.sl) * p.Dh * 2 + piece * kPieceBytes;
-    char* dst = p.dst[g] + tensor * p.tensor_bytes + ((b * p.hl + hh) * p.S + rank * p.sl) * p.Dh * 2 +
+    char* dst = p.dst[par][g] + tensor * p.tensor_bytes + ((b * p.hl + hh) * p.S + rank * p.sl) * p.Dh * 2 +
                 piece * kPieceBytes;
     const int64_t n = min(static_cast<int64_t>(kPieceBytes), block_bytes - piece * kPieceBytes) / 16;
     const int4* s4 = reinterpret_cast<const int4*>(src);
@@ -63,8 +69,9 @@ __global__ void __launch_bounds__(kPushThreads) ulysses_push_kernel(UlyssesParam
   __syncthreads();
   if (threadIdx.x < T && rank != p.fault_rank) {
     __threadfence_system();
-    st_relaxed_sys(p.flags[threadIdx.x] + static_cast<int64_t>(rank) * p.ctas_per_rank + cta, p.epoch);
+    st_relaxed_sys(p.flags[par][threadIdx.x] + static_cast<int64_t>(rank) * p.ctas_per_rank + cta, epoch);
   }
+  if (threadIdx.x == 0) epoch_publish(p.epoch_dev, epoch);
 }
 
 }  // namespace

@@ -789,9 +789,8 @@ def test_ulysses_attention_full_cfg5_vs_sdpa():
             assert err <= 2e-2 * ref.float().abs().max().item() + 2e-3, (r, grp, err)
 
 
-def test_cuda_graph_capture_policy():
-    """Single-rank calls capture into a CUDA graph and replay correctly; multi-rank fused
-    collectives refuse capture loudly (their per-call epochs are host-side)."""
+def test_cuda_graph_capture_single_rank():
+    """Single-rank calls capture into a CUDA graph and replay correctly."""
     g = torch.Generator(device=DEV).manual_seed(4)
     a = torch.randn((512, 256), device=DEV, generator=g).to(torch.bfloat16)
     b = torch.randn((256, 384), device=DEV, generator=g).to(torch.bfloat16)
@@ -807,12 +806,84 @@ def test_cuda_graph_capture_policy():
     torch.cuda.synchronize()
     assert torch.allclose(c, a.float() @ b.float(), rtol=1e-3, atol=1e-2)
 
-    comm = tpf.Communicator.local_group(2, tpf.sym_bytes_rs(2, 1, 256, 128, 256, 1))
-    x = torch.zeros((2, 1, 256, 128), device=DEV, dtype=torch.bfloat16)
-    w = torch.zeros((2, 128, 256), device=DEV, dtype=torch.bfloat16)
-    y = torch.zeros((2, 1, 128, 256), device=DEV)
+
+@pytest.mark.parametrize("T", [2, 4])
+def test_cuda_graph_capture_fused_collectives(T):
+    """Multi-rank fused collectives are graph-replayable: the call's epoch and heap parity live
+    in device memory, so every replay advances them. A captured MLP block (AG-GEMM + GEMM-RS)
+    is replayed with fresh inputs, interleaved with eager calls on the same communicator, and
+    must match the oracle bit for bit on integer data every time."""
+    B, S, D, H = 1, 256 * T, 256, 512
+    s = torch.cuda.Stream(DEV)
+    comm = tpf.Communicator.local_group(T, max(tpf.sym_bytes_ag(T, B, S, D, H // T), tpf.sym_bytes_rs(T, B, S, H // T, D)))
+    x = torch.zeros((T, B, S // T, D), device=DEV, dtype=torch.bfloat16)
+    up = O.randint((D, H), -1, 2, 31)   # |hidden| <= 256: exact after the bf16 re-cast
+    down = O.randint((H, D), -2, 3, 32)
+    wu = torch.stack([bf16(up[:, r * (H // T):(r + 1) * (H // T)]) for r in range(T)]).to(DEV)
+    wd = torch.stack([bf16(down[r * (H // T):(r + 1) * (H // T)]) for r in range(T)]).to(DEV)
+    hid = torch.empty((T, B, S, H // T), device=DEV, dtype=torch.float32)
+    hid_b = torch.empty((T, B, S, H // T), device=DEV, dtype=torch.bfloat16)
+    y = torch.empty((T, B, S // T, D), device=DEV, dtype=torch.float32)
+
+    def block():
+        comm.ag_gemm(x, wu, hid, stream=s)
+        hid_b.copy_(hid)
+        comm.gemm_rs(hid_b, wd, y, kind=tpf.RING, stream=s)
+
+    with torch.cuda.stream(s):
+        block()  # warm-up outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        block()
+    for rep in range(4):
+        xf = O.randint((B, S, D), 0, 2, 40 + rep)
+        x.copy_(torch.stack([bf16(xf[:, r * (S // T):(r + 1) * (S // T)]) for r in range(T)]))
+        graph.replay()
+        torch.cuda.synchronize()
+        want_h = O.column_parallel(T, 1, xf, up)
+        assert np.array_equal(hid.double().cpu().numpy(), want_h), rep
+        want = O.row_parallel(T, tpf.RING, 1, np.concatenate(list(want_h), axis=-1), down)
+        assert np.array_equal(y.double().cpu().numpy(), want), rep
+        if rep == 1:  # an eager call between replays advances the same device epoch
+            with torch.cuda.stream(s):
+                block()
+            torch.cuda.synchronize()
+            assert np.array_equal(y.double().cpu().numpy(), want)
+    comm.close()
+
+
+def test_cuda_graph_capture_attention_paths():
+    """The fused attention all-to-all and the whole Ulysses layer replay from a graph and match
+    their eager results; the unfused fallback (head_dim != 128) refuses capture loudly."""
+    T, batch, heads, sl, Dh = 2, 1, 4, 256, 128
+    S = sl * T
+    g = torch.Generator(device=DEV).manual_seed(8)
+    xs = [torch.randn((T, batch * heads, sl, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
+    hs = [torch.randn((T, batch * heads // T, S, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
+    o1 = torch.empty((T, batch, sl, heads * Dh), device=DEV, dtype=torch.bfloat16)
+    o2 = torch.empty_like(o1)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, heads, S, Dh))
+    s = torch.cuda.Stream(DEV)
+    with torch.cuda.stream(s):
+        comm.ulysses_attention(*xs, o1, batch, heads, stream=s)
+        comm.attention_a2a(*hs, o2, batch, heads // T, stream=s)
+    torch.cuda.synchronize()
+    e1, e2 = o1.clone(), o2.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        comm.ulysses_attention(*xs, o1, batch, heads, stream=s)
+        comm.attention_a2a(*hs, o2, batch, heads // T, stream=s)
+    for _ in range(3):
+        o1.zero_()
+        o2.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(o1, e1) and torch.equal(o2, e2)
+    q32 = torch.zeros((T, batch * 2, S, 32), device=DEV, dtype=torch.bfloat16)
+    o32 = torch.zeros((T, batch, sl, T * 2 * 32), device=DEV, dtype=torch.bfloat16)
     graph2 = torch.cuda.CUDAGraph()
     with pytest.raises(ValueError, match="CUDA graph"):
         with torch.cuda.graph(graph2, stream=s):
-            comm.gemm_rs(x, w, y, stream=s)
+            comm.attention_a2a(q32, q32, q32, o32, batch, 2, stream=s)
     comm.close()
