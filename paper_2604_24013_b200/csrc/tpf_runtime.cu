@@ -140,7 +140,6 @@ struct tpf_comm {
   char* sym[tpf::kMaxRanks] = {};
   bool opened[tpf::kMaxRanks] = {};
   bool peers_ready = false;
-  uint32_t epoch = 0;           // host mirror, used only by the unfused attention fallback
   uint32_t* dev_epoch = nullptr;  // device epoch [value, exit counter] (graph-replayable calls)
   uint32_t* err = nullptr;      // device error record
   int64_t timeout_ns = kDefaultTimeoutNs;
@@ -175,15 +174,15 @@ int64_t data_bytes_per_parity(size_t sym_bytes) {
   return (static_cast<int64_t>(sym_bytes) - 2 * kFlagBytesPerParity) / 2;
 }
 
-// Multi-rank calls take their epoch (flag value) and heap parity from a host counter, so a
-// captured CUDA graph would replay stale epochs and pass every flag wait on old data.
-// Refuse capture loudly instead (single-rank calls have no flags and may be captured).
+// The unfused attention fallback reads the device epoch back to the host to build its
+// multi-launch pointers, which a captured CUDA graph cannot replay. It refuses capture
+// loudly (everything else keeps the epoch on the device and is graph-replayable).
 tpf::Status check_not_capturing(const tpf_comm* c, cudaStream_t stream) {
   if (!c || c->world <= 1) return tpf::Status::ok();
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(stream, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone)
-    return tpf::Status::invalid("multi-rank fused collectives cannot be captured into a CUDA graph "
-                                "(per-call epochs are host-side); capture only single-rank calls");
+    return tpf::Status::invalid("the unfused attention fallback (head_dim != 128) cannot be captured into a "
+                                "CUDA graph (host-side epoch read); use head_dim 128 or call it eagerly");
   return tpf::Status::ok();
 }
 
