@@ -1,6 +1,8 @@
 """Soak test: one communicator, a seeded random sequence of every fused operator (both heap
 parities, every schedule, graph replays in between), each result checked. Catches any
 cross-operator interference through the shared flag / heap regions and the device epoch."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -12,7 +14,9 @@ pytestmark = pytest.mark.gpu
 
 
 def test_mixed_operator_sequence_on_one_communicator():
-    T, B, S, D, H = 4, 1, 512, 256, 512
+    # TPF_SOAK="T,steps" for a longer run (default 4 ranks, 40 steps)
+    T, steps = (int(v) for v in os.environ.get("TPF_SOAK", "4,40").split(","))
+    B, S, D, H = 1, 128 * T, 256, 128 * T
     heads, Dh = 4, 128
     rng = np.random.default_rng(2027)
     need = max(tpf.sym_bytes_ag(T, B, S, D, H // T), tpf.sym_bytes_rs(T, B, S, H // T, D, 2),
@@ -81,7 +85,7 @@ def test_mixed_operator_sequence_on_one_communicator():
         run_ag(comm)
         run_rs(comm, tpf.RING, 1)
 
-    for step in range(40):
+    for step in range(steps):
         if step % 7 == 3:
             out_ag.zero_()
             out_rs.zero_()
