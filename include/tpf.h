@@ -211,8 +211,10 @@ int64_t tpf_sym_bytes_ulysses(int world, int64_t batch, int64_t heads_total, int
  *   q, k, v : bf16 (batch*heads, S, 128)  this rank's head group, full sequence
  *   w_o     : bf16 (heads*128, D)         this rank's row shard of the output projection
  *   out     : (batch, S/T, D) out_dtype
- * The attention context of every slice comes from one fused tcgen05 flash-attention launch;
- * the projection + reduce-scatter is the fused GEMM-RS (schedule reduction order). */
+ * The attention produces the context slice by slice in the RS schedule's order on part of the
+ * SMs while, on a second stream, the fused GEMM-RS consumes each finished slice (per-slice
+ * ready counters) on the rest: projection and transfer of step i run under the attention of
+ * the later slices (Alg. 4). The reduction order is the schedule's. Graph-capturable. */
 int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const void* v, const void* w_o,
                               void* out, int64_t batch, int64_t heads, int64_t S, int64_t Dh, int64_t D, int kind,
                               int wire_dtype, int out_dtype, int scale, void* stream);

@@ -185,7 +185,9 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       for (int it = c; it < nitems; it += C, ++ic) {
         const int step = it / per_step, rem = it - step * per_step;
         const int g = rem / npair, pr = rem - g * npair;
-        const int l = p.local ? 0 : (rank + step + 1) % p.T;
+        // query slice of this step: UP sends slice (r+i+1) % T; query-split follows the RS
+        // schedule's slice order; plain local attention has a single slice
+        const int l = p.qsplit ? p.slice_of[h][step] : p.local ? 0 : (rank + step + 1) % p.T;
         const int row0 = static_cast<int>(static_cast<int64_t>(l) * p.sl + pr * 2 * kFTile);
         fmha_wait(p, q_empty, (ic & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, 2 * kFTileBytes);
@@ -294,6 +296,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       const int g = rem / npair, pr = rem - g * npair;
       const int qt = pr * 2 + w;
       const int dst = p.local ? rank : (rank + step + 1) % p.T;
+      const int l = p.qsplit ? p.slice_of[h][step] : 0;
       float m = -INFINITY, lsum = 0.f;
       for (int j = 0; j < p.nkv; ++j, ++sc) {
         fmha_wait(p, s_full + w, sc & 1);
@@ -388,7 +391,8 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         const float inv = 1.f / lsum;
         const int b = g / p.heads, hh = g - b * p.heads;
         char* orow = p.recv[par][dst] +
-                     ((static_cast<int64_t>(b) * p.sl + qt * kFTile + row) * p.fw +
+                     ((static_cast<int64_t>(b) * (p.qsplit ? p.S : p.sl) + (p.qsplit ? l * p.sl : 0) +
+                       qt * kFTile + row) * p.fw +
                       (static_cast<int64_t>(p.local ? 0 : rank) * p.heads + hh) * kFTile) * 2;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -413,6 +417,13 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
                                (static_cast<int64_t>(g) * p.nqt + qt) * 4 + ew,
                            epoch);
         }
+      }
+      if (p.qsplit) {
+        // query-split: this warp's 32 context rows of slice l are stored; the concurrently
+        // running GEMM-RS waits for all of the slice's warps (phantom tiles count too)
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(p.qs_ready[h] + l, 1u);
       }
       // O_w is read (tcgen05.ld waited) before this warp's next p_ready arrival, and PV_w(0)
       // of the next item is issued only after that arrival.

@@ -28,6 +28,8 @@ enum Mode : int {
   MODE_QK = 3,        // B K-major, per batch (head); per-rank A row offset: UP scores
   MODE_PV = 4,        // B MN-major, per batch; merge_heads + peer push + flags: UP output
   MODE_SINGLE = 5,    // MODE_STD operands, T == 1 (no ring): the degenerate GEMM (+ epilogue act)
+  MODE_QSPLIT = 6,    // GEMM-RS whose A slices are produced concurrently by the attention kernel:
+                      // a step's tiles wait for their query slice's ready counter (Alg. 4)
 };
 
 // Error record in device memory (first error wins).
@@ -86,6 +88,8 @@ struct KParams {
   int64_t flags_per_slot;
   uint32_t epoch;      // static epoch / parity, used when epoch_dev is null (T == 1 calls)
   int parity;
+  const uint32_t* qs_ready[kMaxRanks];  // MODE_QSPLIT: per hosted rank, per query slice counters
+  uint32_t qs_target;                   // MODE_QSPLIT: counter value of a finished slice
   uint32_t* epoch_dev; // device epoch [value, exit counter]: read at entry (+ epoch_bump), and
   int epoch_bump;      // the last CTA to exit publishes the value (CUDA-graph replayable)
   int8_t sched[kMaxRanks][kMaxRanks][3];  // [rank][step] (send, recv, slice)
@@ -124,6 +128,9 @@ struct FmhaParams {
   int parity;
   uint32_t* epoch_dev;                 // device epoch (see KParams)
   int epoch_bump;
+  int qsplit;                          // query-split: local context in the RS schedule's slice
+  int8_t slice_of[kMaxRanks][kMaxRanks];  // order ([hosted rank][step] -> slice), and one
+  uint32_t* qs_ready[kMaxRanks];       // counter per (hosted rank, slice) bumped per finished warp
   int fault_rank;
   uint32_t* err;
   int64_t timeout_ns;

@@ -387,6 +387,24 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       uint64_t t_first = 0;
       const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
       const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
+      if (kMode == MODE_QSPLIT && t.valid > 0 && lane == 0 && !p.compute_only) {
+        // the A rows of this step's query slice come from the concurrently running attention
+        // kernel (generic stores): wait for the slice's counter, then order the TMA reads
+        const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
+        const uint32_t* cnt = p.qs_ready[h] + l;
+        if (ld_acquire_gpu(cnt) < p.qs_target) {
+          const uint64_t tq0 = globaltimer();
+          while (ld_acquire_gpu(cnt) < p.qs_target) {
+            if (aborted(p)) break;
+            if (globaltimer() - tq0 > static_cast<uint64_t>(p.timeout_ns)) {
+              record_error(p, 1, rank, t.step, lin);
+              break;
+            }
+            __nanosleep(256);
+          }
+        }
+        fence_proxy_async_global();
+      }
       for (int kb = 0; kb < p.nkb; ++kb) {
         if (wire_live && kb > ready) {
           // Wait for image kb, then claim the run of consecutive landed images: every lane
@@ -778,6 +796,7 @@ void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
     case MODE_GATHER_B: launch_instance<OP_AG, MODE_GATHER_B>(p, grid, stream); return;
     case MODE_QK: launch_instance<OP_RS, MODE_QK>(p, grid, stream); return;
     case MODE_PV: launch_instance<OP_RS, MODE_PV>(p, grid, stream); return;
+    case MODE_QSPLIT: launch_instance<OP_RS, MODE_QSPLIT>(p, grid, stream); return;
     case MODE_SINGLE:
       if (p.op == OP_AG) launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream);
       else launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);

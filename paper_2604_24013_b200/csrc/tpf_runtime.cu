@@ -141,6 +141,9 @@ struct tpf_comm {
   bool opened[tpf::kMaxRanks] = {};
   bool peers_ready = false;
   uint32_t* dev_epoch = nullptr;  // device epoch [value, exit counter] (graph-replayable calls)
+  uint32_t* qs_ready = nullptr;   // query-split slice counters [hosted rank][slice]
+  cudaStream_t side = nullptr;    // query-split: the GEMM-RS runs here, concurrently with attention
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   uint32_t* err = nullptr;      // device error record
   int64_t timeout_ns = kDefaultTimeoutNs;
   int device = 0;
@@ -201,6 +204,9 @@ struct Call {
   int64_t out_col_off[tpf::kMaxRanks];
   uint32_t* done_rank[tpf::kMaxRanks];
   bool no_epoch;   // do not advance the epoch (steps of one multi-launch collective)
+  int max_pairs_per_rank;                        // 0: all resident CTA pairs
+  const uint32_t* qs_ready[tpf::kMaxRanks];      // non-null: MODE_QSPLIT (A slices from the attention)
+  uint32_t qs_target;
   const void* x;
   const void* w;
   void* out;
@@ -265,6 +271,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
          : k.gather_b ? tpf::MODE_GATHER_B
          : (k.b_batched && k.b_kmajor) ? tpf::MODE_QK
          : k.b_batched ? tpf::MODE_PV
+         : k.qs_ready[0] ? tpf::MODE_QSPLIT
          : k.T == 1 ? tpf::MODE_SINGLE
          : tpf::MODE_STD;
   if ((p.mode == tpf::MODE_STD || p.mode == tpf::MODE_SINGLE) && k.b_kmajor)
@@ -295,6 +302,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.nnt = g.nnt;
   p.nkb = g.nkb;
   p.npairs = g.npairs;
+  for (int h = 0; h < R; ++h) p.qs_ready[h] = k.qs_ready[h];
+  p.qs_target = k.qs_target;
   p.group_m = env_group_m();
   p.ag_nfwd = env_int("TPF_AG_NFWD", 4);
   p.ag_batch = env_int("TPF_AG_BATCH", 4);
@@ -383,7 +392,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   int pairs = tpf::max_pairs();
   if (pairs <= 0) return tpf::Status::cuda("kernel cannot be resident (cluster occupancy 0)");
   pairs = std::min(pairs, sms / 2);
-  const int pairs_per_rank = pairs / R;
+  int pairs_per_rank = pairs / R;
+  if (k.max_pairs_per_rank > 0) pairs_per_rank = std::min(pairs_per_rank, k.max_pairs_per_rank);
   if (pairs_per_rank < 1)
     return tpf::Status::invalid("local group of " + std::to_string(R) + " ranks needs " +
                                 std::to_string(R) + " resident CTA pairs, device has " +
@@ -461,6 +471,10 @@ int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out) {
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->qs_ready, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
@@ -519,6 +533,10 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
   if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->qs_ready, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
@@ -541,6 +559,10 @@ int tpf_comm_destroy(tpf_comm* c) {
   if (c->local) cudaFree(c->local);
   if (c->err) cudaFree(c->err);
   if (c->dev_epoch) cudaFree(c->dev_epoch);
+  if (c->qs_ready) cudaFree(c->qs_ready);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->scratch) cudaFree(c->scratch);
   delete c;
   return TPF_OK;
@@ -911,9 +933,10 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
     if (s.good()) s = make_tmap(&fp.tmap_v[par], v, 4, dims, strides, box);
   }
   if (!s.good()) return fail(s);
-  fp.T = 1; fp.local = 1; fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
-  fp.nqt = static_cast<int>(S / 128); fp.nkv = static_cast<int>(S / 128);
-  fp.S = S; fp.sl = S; fp.fw = hd;
+  fp.R = R; fp.rank0 = r0; fp.heads = static_cast<int>(heads); fp.G = static_cast<int>(G);
+  fp.local = 1;
+  fp.nkv = static_cast<int>(S / 128);
+  fp.S = S; fp.fw = hd;
   fp.scale_log2 = (scale ? 1.0f / std::sqrt(static_cast<float>(Dh)) : 1.0f) * 1.4426950408889634f;
   for (int hh = 0; hh < R; ++hh)
     fp.recv[0][r0 + hh] = fp.recv[1][r0 + hh] = c->scratch + static_cast<size_t>(hh) * batch * S * hd * 2;
@@ -921,9 +944,6 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   fp.err = c->err;
   fp.timeout_ns = c->timeout_ns;
   fp.fault_rank = -1;
-  const int sms = tpf::num_sms();
-  fp.ctas_per_rank = std::max(1, sms / R);
-  TPF_CUDA_TRY(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
   Call kc{};
   kc.op = tpf::OP_RS;
   kc.T = T;
@@ -936,8 +956,45 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   kc.B = batch; kc.Sc = S / T; kc.K = hd; kc.N = D; kc.x_rows = S; kc.out_rows = S / T;
   kc.x = c->scratch; kc.w = w_o; kc.out = out;
   kc.sched = T > 1 ? sched.data() : nullptr;
-  s = launch(c, kc, stream);
-  return s.good() ? TPF_OK : fail(s);
+  const int sms = tpf::num_sms();
+  const int64_t sl = S / T;
+  // Alg. 4 proper: the attention produces the query slices in the RS schedule's order on part
+  // of the SMs while the GEMM-RS consumes them on the rest, so each step's projection and
+  // transfer ride under the attention of the next slices. The split follows the work ratio.
+  const double attn_t = 4.0 * G * S * S * Dh * 1.15, proj_t = 2.0 * batch * S * hd * D;
+  const int per_rank = sms / R;
+  int rs_pairs = static_cast<int>(std::lround(proj_t / (attn_t + proj_t) * per_rank / 2.0));
+  rs_pairs = std::max(1, std::min(rs_pairs, per_rank / 2 - 1));
+  const int fmha_ctas = per_rank - 2 * rs_pairs;
+  const bool concurrent = T > 1 && sl % 128 == 0 && fmha_ctas >= 1 && env_int("TPF_QSPLIT_CONCURRENT", 1) != 0;
+  if (!concurrent) {
+    fp.T = 1; fp.sl = S; fp.nqt = static_cast<int>(S / 128);
+    fp.ctas_per_rank = std::max(1, per_rank);
+    TPF_CUDA_TRY(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
+    s = launch(c, kc, stream);
+    return s.good() ? TPF_OK : fail(s);
+  }
+  fp.T = T; fp.sl = sl; fp.nqt = static_cast<int>(sl / 128);
+  fp.qsplit = 1;
+  for (int hh = 0; hh < R; ++hh) {
+    for (int i = 0; i < T; ++i) fp.slice_of[hh][i] = static_cast<int8_t>(sched[((r0 + hh) * T + i) * 3 + 2]);
+    fp.qs_ready[hh] = c->qs_ready + hh * tpf::kMaxRanks;
+    kc.qs_ready[hh] = fp.qs_ready[hh];
+  }
+  kc.qs_target = static_cast<uint32_t>(G * ((fp.nqt + 1) / 2) * 8);  // items x 2 tiles x 4 warps
+  kc.max_pairs_per_rank = rs_pairs;
+  fp.ctas_per_rank = fmha_ctas;
+  TPF_CUDA_TRY(cudaMemsetAsync(c->qs_ready, 0, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t), stream));
+  TPF_CUDA_TRY(cudaEventRecord(c->ev_fork, stream));
+  TPF_CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  TPF_CUDA_TRY(tpf::launch_fmha_a2a(fp, fp.ctas_per_rank * R, stream));
+  // Deadlock-free by construction: the attention never waits on the GEMM-RS, so every CTA of
+  // it finishes even if some GEMM-RS clusters only become resident after it.
+  s = launch(c, kc, c->side);
+  if (!s.good()) return fail(s);
+  TPF_CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+  TPF_CUDA_TRY(cudaStreamWaitEvent(stream, c->ev_join, 0));
+  return TPF_OK;
 }
 
 int tpf_gemm(const void* a, const void* b, void* out, int64_t M, int64_t K, int64_t N,

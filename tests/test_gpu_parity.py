@@ -880,6 +880,22 @@ def test_cuda_graph_capture_attention_paths():
         graph.replay()
         torch.cuda.synchronize()
         assert torch.equal(o1, e1) and torch.equal(o2, e2)
+    # query-split attention: attention and GEMM-RS run concurrently on two streams (event
+    # fork / join), which the capture must reproduce
+    w_o = (torch.randn((T, (heads // T) * Dh, 256), device=DEV, generator=g) / 16).to(torch.bfloat16)
+    o3 = torch.empty((T, batch, sl, 256), device=DEV)
+    with torch.cuda.stream(s):
+        comm.query_split_attention(*hs, w_o, o3, batch, heads // T, stream=s)
+    torch.cuda.synchronize()
+    e3 = o3.clone()
+    graph3 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph3, stream=s):
+        comm.query_split_attention(*hs, w_o, o3, batch, heads // T, stream=s)
+    for _ in range(3):
+        o3.zero_()
+        graph3.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(o3, e3)
     q32 = torch.zeros((T, batch * 2, S, 32), device=DEV, dtype=torch.bfloat16)
     o32 = torch.zeros((T, batch, sl, T * 2 * 32), device=DEV, dtype=torch.bfloat16)
     graph2 = torch.cuda.CUDAGraph()
