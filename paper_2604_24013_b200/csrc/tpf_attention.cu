@@ -110,6 +110,9 @@ __device__ __forceinline__ void fmha_wait(const FmhaParams& p, uint64_t* bar, ui
 
 }  // namespace
 
+// kQSplit: query-split instance (slice order from the RS schedule, per-slice ready counters);
+// a compile-time switch so the UP / plain instance carries none of its code.
+template <bool kQSplit>
 __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_constant__ FmhaParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -187,7 +190,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         const int g = rem / npair, pr = rem - g * npair;
         // query slice of this step: UP sends slice (r+i+1) % T; query-split follows the RS
         // schedule's slice order; plain local attention has a single slice
-        const int l = p.qsplit ? p.slice_of[h][step] : p.local ? 0 : (rank + step + 1) % p.T;
+        const int l = kQSplit ? p.slice_of[h][step] : p.local ? 0 : (rank + step + 1) % p.T;
         const int row0 = static_cast<int>(static_cast<int64_t>(l) * p.sl + pr * 2 * kFTile);
         fmha_wait(p, q_empty, (ic & 1) ^ 1);
         mbar_arrive_expect_tx(q_full, 2 * kFTileBytes);
@@ -296,7 +299,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
       const int g = rem / npair, pr = rem - g * npair;
       const int qt = pr * 2 + w;
       const int dst = p.local ? rank : (rank + step + 1) % p.T;
-      const int l = p.qsplit ? p.slice_of[h][step] : 0;
+      const int l = kQSplit ? p.slice_of[h][step] : 0;
       float m = -INFINITY, lsum = 0.f;
       for (int j = 0; j < p.nkv; ++j, ++sc) {
         fmha_wait(p, s_full + w, sc & 1);
@@ -391,7 +394,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
         const float inv = 1.f / lsum;
         const int b = g / p.heads, hh = g - b * p.heads;
         char* orow = p.recv[par][dst] +
-                     ((static_cast<int64_t>(b) * (p.qsplit ? p.S : p.sl) + (p.qsplit ? l * p.sl : 0) +
+                     ((static_cast<int64_t>(b) * (kQSplit ? p.S : p.sl) + (kQSplit ? l * p.sl : 0) +
                        qt * kFTile + row) * p.fw +
                       (static_cast<int64_t>(p.local ? 0 : rank) * p.heads + hh) * kFTile) * 2;
 #pragma unroll
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
                            epoch);
         }
       }
-      if (p.qsplit) {
+      if (kQSplit) {
         // query-split: this warp's 32 context rows of slice l are stored; the concurrently
         // running GEMM-RS waits for all of the slice's warps (phantom tiles count too)
         __threadfence();
@@ -438,20 +441,25 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, epoch);
 }
 
-cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream) {
+template <bool kQSplit>
+cudaError_t launch_fmha_instance(const FmhaParams& p, int grid, cudaStream_t stream) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, tpf_fmha_a2a_kernel);
+    cudaError_t e = cudaFuncGetAttributes(&fa, tpf_fmha_a2a_kernel<kQSplit>);
     if (e != cudaSuccess) return e;
     // the setmaxnreg split above must fit the pool the launch allocates, or the kernel hangs
     if (fa.numRegs * 384 < 72 * 128 + 216 * 256) return cudaErrorInvalidConfiguration;
-    e = cudaFuncSetAttribute(tpf_fmha_a2a_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+    e = cudaFuncSetAttribute(tpf_fmha_a2a_kernel<kQSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  tpf_fmha_a2a_kernel<<<grid, 384, kFSmem, stream>>>(p);
+  tpf_fmha_a2a_kernel<kQSplit><<<grid, 384, kFSmem, stream>>>(p);
   return cudaGetLastError();
+}
+
+cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream) {
+  return p.qsplit ? launch_fmha_instance<true>(p, grid, stream) : launch_fmha_instance<false>(p, grid, stream);
 }
 
 }  // namespace tpf
