@@ -1,4 +1,5 @@
-"""B200-native CommFuse hot path (arXiv 2604.24013): fused AG-GEMM / GEMM-RS.
+"""B200-native CommFuse hot path (arXiv 2604.24013): fused AG-GEMM / GEMM-RS, the DP
+gradient / parameter collectives, and the fused attention all-to-alls (Ulysses, query-split).
 
 Python host mirror of the reference's operator API for this path
 (/root/reference/proj/include/tpfuse/{collectives,layers}.hpp) over the C ABI
@@ -278,6 +279,58 @@ class Communicator:
         _check(_lib.tpf_gemm_rs(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B, S, K, N,
                                 kind, m, wire, _dtype_code(out), _stream_ptr(stream)))
 
+    def dp_grad_rs(self, X, dY, dW, kind: int = RING, m: int = 1, wire: int = F32, stream=None) -> None:
+        """DP gradient reduce-scatter fused into the weight-gradient GEMM (cfg 4):
+        dW_r = rows [r*K/T, (r+1)*K/T) of sum_q X_q^T dY_q. Per rank X: (M_local, K), dY: (M_local, N),
+        dW: (K/T, N); a local group takes rank-stacked tensors."""
+        M_local, K = X.shape[-2:]
+        N = dY.shape[-1]
+        _check(_lib.tpf_dp_grad_rs(self._h, X.data_ptr(), dY.data_ptr(), dW.data_ptr(), M_local, K, N, kind, m,
+                                   wire, _dtype_code(dW), _stream_ptr(stream)))
+
+    def dp_param_ag_gemm(self, x, w_rows, out, stream=None) -> None:
+        """DP parameter all-gather fused into the forward GEMM (cfg 4, a19): out = x . W^T where
+        W (N x K) is row-sharded over the ranks (PyTorch Linear layout). Per rank x: (M_local, K),
+        w_rows: (N/T, K), out: (M_local, N); a local group takes rank-stacked tensors."""
+        M_local, K = x.shape[-2:]
+        N_local = w_rows.shape[-2]
+        _check(_lib.tpf_dp_param_ag_gemm(self._h, x.data_ptr(), w_rows.data_ptr(), out.data_ptr(), M_local, K,
+                                         N_local, _dtype_code(out), _stream_ptr(stream)))
+
+    def attention_a2a(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
+        """fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218; BASELINE cfg 5).
+        Per rank q/k/v: (batch*heads, S, Dh) bf16; out: (batch, S/T, T*heads*Dh) bf16.
+        A local group takes rank-stacked tensors."""
+        S, Dh = q.shape[-2:]
+        _check(_lib.tpf_attention_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch, heads,
+                                      S, Dh, int(bool(scale)), _stream_ptr(stream)))
+
+    def query_split_attention(self, q, k, v, w_o, out, batch: int, heads: int, kind: int = RING,
+                               wire: int = F32, scale: bool = True, stream=None) -> None:
+        """query_split_attention (Alg. 4, layers.cpp:149-172). Per rank q/k/v: (batch*heads, S, 128)
+        bf16, w_o: (heads*128, D) bf16 (row shard), out: (batch, S/T, D). Local groups: rank-stacked."""
+        S, Dh = q.shape[-2:]
+        D = w_o.shape[-1]
+        _check(_lib.tpf_query_split_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), w_o.data_ptr(),
+                                              out.data_ptr(), batch, heads, S, Dh, D, kind, wire, _dtype_code(out),
+                                              int(bool(scale)), _stream_ptr(stream)))
+
+    def ulysses_a2a(self, q, k, v, q_out, k_out, v_out, batch: int, heads: int, stream=None) -> None:
+        """Ulysses first all-to-all (ref_all_to_all of layers_test.cpp:347-397):
+        per rank q/k/v (batch*heads, S/T, Dh) bf16 with every head -> (batch*heads/T, S, Dh), this
+        rank's head group over the whole sequence. Local groups: rank-stacked."""
+        sl, Dh = q.shape[-2:]
+        _check(_lib.tpf_ulysses_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), q_out.data_ptr(),
+                                    k_out.data_ptr(), v_out.data_ptr(), batch, heads, sl * self.world, Dh,
+                                    _stream_ptr(stream)))
+
+    def ulysses_attention(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
+        """The whole UP attention (Alg. 5 with its first all-to-all): sequence-sharded q/k/v
+        (batch*heads, S/T, 128) per rank -> out (batch, S/T, heads*128), with both all-to-alls fused
+        (peer-store inbox + fused flash attention pushing O tiles to the slice owner)."""
+        sl, Dh = q.shape[-2:]
+        _check(_lib.tpf_ulysses_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch,
+                                          heads, sl * self.world, Dh, int(bool(scale)), _stream_ptr(stream)))
 
 def interleave_gate_up(gate, up, tile: int = 256):
     """Tile-interleaved gate||up shard for the fused SwiGLU epilogue (ACT_SWIGLU):
@@ -289,83 +342,6 @@ def interleave_gate_up(gate, up, tile: int = 256):
     assert up.shape == gate.shape and F % half == 0
     return torch.stack([gate.reshape(K, F // half, half), up.reshape(K, F // half, half)],
                        dim=2).reshape(K, 2 * F)
-
-
-def _dp_grad_rs(self, X, dY, dW, kind: int = RING, m: int = 1, wire: int = F32, stream=None) -> None:
-    """DP gradient reduce-scatter fused into the weight-gradient GEMM (cfg 4):
-    dW_r = rows [r*K/T, (r+1)*K/T) of sum_q X_q^T dY_q. Per rank X: (M_local, K), dY: (M_local, N),
-    dW: (K/T, N); a local group takes rank-stacked tensors."""
-    M_local, K = X.shape[-2:]
-    N = dY.shape[-1]
-    _check(_lib.tpf_dp_grad_rs(self._h, X.data_ptr(), dY.data_ptr(), dW.data_ptr(), M_local, K, N, kind, m,
-                               wire, _dtype_code(dW), _stream_ptr(stream)))
-
-
-Communicator.dp_grad_rs = _dp_grad_rs
-
-
-def _dp_param_ag_gemm(self, x, w_rows, out, stream=None) -> None:
-    """DP parameter all-gather fused into the forward GEMM (cfg 4, a19): out = x . W^T where
-    W (N x K) is row-sharded over the ranks (PyTorch Linear layout). Per rank x: (M_local, K),
-    w_rows: (N/T, K), out: (M_local, N); a local group takes rank-stacked tensors."""
-    M_local, K = x.shape[-2:]
-    N_local = w_rows.shape[-2]
-    _check(_lib.tpf_dp_param_ag_gemm(self._h, x.data_ptr(), w_rows.data_ptr(), out.data_ptr(), M_local, K,
-                                     N_local, _dtype_code(out), _stream_ptr(stream)))
-
-
-Communicator.dp_param_ag_gemm = _dp_param_ag_gemm
-
-
-def _attention_a2a(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
-    """fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218; BASELINE cfg 5).
-    Per rank q/k/v: (batch*heads, S, Dh) bf16; out: (batch, S/T, T*heads*Dh) bf16.
-    A local group takes rank-stacked tensors."""
-    S, Dh = q.shape[-2:]
-    _check(_lib.tpf_attention_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch, heads,
-                                  S, Dh, int(bool(scale)), _stream_ptr(stream)))
-
-
-Communicator.attention_a2a = _attention_a2a
-
-
-def _query_split_attention(self, q, k, v, w_o, out, batch: int, heads: int, kind: int = RING,
-                           wire: int = F32, scale: bool = True, stream=None) -> None:
-    """query_split_attention (Alg. 4, layers.cpp:149-172). Per rank q/k/v: (batch*heads, S, 128)
-    bf16, w_o: (heads*128, D) bf16 (row shard), out: (batch, S/T, D). Local groups: rank-stacked."""
-    S, Dh = q.shape[-2:]
-    D = w_o.shape[-1]
-    _check(_lib.tpf_query_split_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), w_o.data_ptr(),
-                                          out.data_ptr(), batch, heads, S, Dh, D, kind, wire, _dtype_code(out),
-                                          int(bool(scale)), _stream_ptr(stream)))
-
-
-Communicator.query_split_attention = _query_split_attention
-
-
-def _ulysses_a2a(self, q, k, v, q_out, k_out, v_out, batch: int, heads: int, stream=None) -> None:
-    """Ulysses first all-to-all (ref_all_to_all of layers_test.cpp:347-397):
-    per rank q/k/v (batch*heads, S/T, Dh) bf16 with every head -> (batch*heads/T, S, Dh), this
-    rank's head group over the whole sequence. Local groups: rank-stacked."""
-    sl, Dh = q.shape[-2:]
-    _check(_lib.tpf_ulysses_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), q_out.data_ptr(),
-                                k_out.data_ptr(), v_out.data_ptr(), batch, heads, sl * self.world, Dh,
-                                _stream_ptr(stream)))
-
-
-Communicator.ulysses_a2a = _ulysses_a2a
-
-
-def _ulysses_attention(self, q, k, v, out, batch: int, heads: int, scale: bool = True, stream=None) -> None:
-    """The whole UP attention (Alg. 5 with its first all-to-all): sequence-sharded q/k/v
-    (batch*heads, S/T, 128) per rank -> out (batch, S/T, heads*128), with both all-to-alls fused
-    (peer-store inbox + fused flash attention pushing O tiles to the slice owner)."""
-    sl, Dh = q.shape[-2:]
-    _check(_lib.tpf_ulysses_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch,
-                                      heads, sl * self.world, Dh, int(bool(scale)), _stream_ptr(stream)))
-
-
-Communicator.ulysses_attention = _ulysses_attention
 
 
 def sym_bytes_ulysses(world, batch, heads, S, Dh=128) -> int:
