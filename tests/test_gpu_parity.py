@@ -694,7 +694,7 @@ def test_ulysses_first_a2a_full_cfg5_exact():
         assert torch.equal(o, want)
 
 
-@pytest.mark.parametrize("op", ["ulysses_a2a", "ulysses_attention", "attention_a2a"])
+@pytest.mark.parametrize("op", ["ulysses_a2a", "ulysses_attention", "attention_a2a", "query_split"])
 def test_failed_rank_raises_group_error_attention(op):
     """A rank that stops publishing in the all-to-all paths surfaces as GroupError, and the
     group recovers for the next call."""
@@ -705,6 +705,8 @@ def test_failed_rank_raises_group_error_attention(op):
     hs = [torch.randn((T, batch * heads // T, S, Dh), device=DEV, generator=g).to(torch.bfloat16) for _ in range(3)]
     outs = [torch.empty((T, batch * heads // T, S, Dh), device=DEV, dtype=torch.bfloat16) for _ in range(3)]
     o = torch.empty((T, batch, sl, heads * Dh), device=DEV, dtype=torch.bfloat16)
+    w_o = torch.zeros(((T, (heads // T) * Dh, 256)), device=DEV, dtype=torch.bfloat16)
+    oq = torch.empty((T, batch, sl, 256), device=DEV)
     comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, batch, heads, S, Dh))
     comm.set_timeout_ms(200)
 
@@ -713,8 +715,10 @@ def test_failed_rank_raises_group_error_attention(op):
             comm.ulysses_a2a(*xs, *outs, batch, heads)
         elif op == "ulysses_attention":
             comm.ulysses_attention(*xs, o, batch, heads)
-        else:
+        elif op == "attention_a2a":
             comm.attention_a2a(*hs, o, batch, heads // T)
+        else:  # query-split: attention and GEMM-RS concurrently on two streams
+            comm.query_split_attention(*hs, w_o, oq, batch, heads // T)
         comm.sync()
 
     comm.inject_fault(1)
