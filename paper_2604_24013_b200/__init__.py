@@ -62,6 +62,7 @@ _lib.tpf_ring_indices.argtypes = [C.c_int] * 4 + [_i32p]
 _lib.tpf_schedule_build.argtypes = [C.c_int, C.c_int, _i32p]
 _lib.tpf_schedule_check.argtypes = [C.c_int, C.c_int, _i32p]
 _lib.tpf_comm_create.argtypes = [C.c_int, C.c_int, C.c_size_t, C.POINTER(_vp)]
+_lib.tpf_comm_create_virtual.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
 _lib.tpf_comm_create_local_group.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
 _lib.tpf_comm_ipc_handle.argtypes = [_vp, _vp]
 _lib.tpf_comm_open_peers.argtypes = [_vp, _vp]
@@ -98,6 +99,7 @@ EXPORTED_SYMBOLS = (
     "tpf_schedule_build",
     "tpf_schedule_check",
     "tpf_comm_create",
+    "tpf_comm_create_virtual",
     "tpf_comm_ipc_handle",
     "tpf_comm_open_peers",
     "tpf_comm_create_local_group",
@@ -196,6 +198,15 @@ class Communicator:
         h = C.c_void_p()
         _check(_lib.tpf_comm_create_local_group(world, sym_bytes_per_rank, C.byref(h)))
         return cls(h.value, 0, world, True)
+
+    @classmethod
+    def virtual_group(cls, world: int, sym_bytes: int) -> "Communicator":
+        """Performance-only: rank 0 of a `world`-rank group with virtual peers (every peer wait
+        passes at once, wire data is stale). Per-rank tensors, full-GPU scale; results are
+        meaningless. See tpf_comm_create_virtual."""
+        h = C.c_void_p()
+        _check(_lib.tpf_comm_create_virtual(world, sym_bytes, C.byref(h)))
+        return cls(h.value, 0, world, False)
 
     @classmethod
     def create(cls, rank: int, world: int, sym_bytes: int) -> "Communicator":

@@ -137,6 +137,7 @@ struct tpf_comm {
   int local_group = 0;          // 1: all ranks hosted by this process (single GPU)
   size_t sym_bytes = 0;         // per rank
   char* local = nullptr;        // this process's allocation (all ranks if local_group)
+  char* virtual_peers = nullptr;  // tpf_comm_create_virtual: the heap every virtual peer aliases
   char* sym[tpf::kMaxRanks] = {};
   bool opened[tpf::kMaxRanks] = {};
   bool peers_ready = false;
@@ -551,12 +552,35 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
   return TPF_OK;
 }
 
+int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
+  // Performance-only: rank 0 of a `world`-rank group on this GPU, with every peer virtual.
+  // Peer heaps alias one scratch heap (sends land there), and this rank's flag blocks are
+  // pre-set to 0xFFFFFFFF, so every peer wait passes at once and wire / inbox data is stale.
+  // The kernels run the real protocol instructions at full-GPU scale, which measures what one
+  // GPU of a TP group computes. Results are NOT meaningful.
+  tpf_comm* c = nullptr;
+  int rc = tpf_comm_create(0, world, sym_bytes, &c);
+  if (rc != TPF_OK) return rc;
+  cudaError_t e = cudaMalloc(&c->virtual_peers, c->sym_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->local, 0xFF, 2 * kFlagBytesPerParity);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    tpf_comm_destroy(c);
+    return fail(tpf::Status::cuda(std::string("tpf_comm_create_virtual: ") + cudaGetErrorString(e)));
+  }
+  for (int r = 1; r < world; ++r) c->sym[r] = c->virtual_peers;
+  c->peers_ready = true;
+  *out = c;
+  return TPF_OK;
+}
+
 int tpf_comm_destroy(tpf_comm* c) {
   if (!c) return TPF_OK;
   cudaDeviceSynchronize();
   for (int r = 0; r < c->world; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->sym[r]);
   if (c->local) cudaFree(c->local);
+  if (c->virtual_peers) cudaFree(c->virtual_peers);
   if (c->err) cudaFree(c->err);
   if (c->dev_epoch) cudaFree(c->dev_epoch);
   if (c->qs_ready) cudaFree(c->qs_ready);
