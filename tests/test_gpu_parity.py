@@ -907,3 +907,54 @@ def test_cuda_graph_capture_attention_paths():
         with torch.cuda.graph(graph2, stream=s):
             comm.attention_a2a(q32, q32, q32, o32, batch, 2, stream=s)
     comm.close()
+
+
+def test_ulysses_and_query_split_batch2():
+    """batch > 1 through the whole Ulysses layer and the concurrent query-split path."""
+    T, batch, heads, sl, Dh, D = 2, 2, 4, 256, 128, 256
+    S = sl * T
+    rng = np.random.default_rng(1500)
+    xs = [bf16_round(rng.uniform(-1, 1, (T, batch * heads, sl, Dh))) for _ in range(3)]
+    hs = [O.ulysses_a2a(T, batch, heads, x) for x in xs]
+    want_u = O.attention_a2a(T, batch, heads // T, *hs, True)
+    w_o = bf16_round(rng.uniform(-1, 1, (T * (heads // T) * Dh, D)) / 16)
+    want_q = O.query_split_attention(T, tpf.RING, batch, heads // T, *hs, w_o)
+    dx = [bf16(x).to(DEV) for x in xs]
+    dh = [bf16(x).to(DEV) for x in hs]
+    comm = tpf.Communicator.local_group(T, max(tpf.sym_bytes_ulysses(T, batch, heads, S, Dh),
+                                               tpf.sym_bytes_rs(T, batch, S, (heads // T) * Dh, D, 1) + (1 << 22)))
+    out_u = torch.empty((T, batch, sl, heads * Dh), device=DEV, dtype=torch.bfloat16)
+    comm.ulysses_attention(*dx, out_u, batch, heads)
+    out_q = torch.empty((T, batch, sl, D), device=DEV)
+    comm.query_split_attention(*dh, bf16(w_o.reshape(T, (heads // T) * Dh, D)).to(DEV), out_q, batch, heads // T)
+    comm.sync()
+    comm.close()
+    assert rel_deviation(out_u.double().cpu().numpy(), want_u) <= 2e-2
+    assert rel_deviation(out_q.double().cpu().numpy(), want_q) <= 2e-2
+
+
+def test_virtual_group_runs_every_operator():
+    """The performance-only virtual group runs each fused operator to completion (no waits
+    can block: peer flags are pre-set) and leaves the communicator usable."""
+    T, S, D, H = 8, 1024, 256, 1024
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, D, H // T),
+                                                 tpf.sym_bytes_rs(T, 1, S, H // T, D, 1),
+                                                 tpf.sym_bytes_ulysses(T, 1, 8 * T, S, 128)))
+    comm.set_timeout_ms(2000)
+    x = torch.zeros((1, S // T, D), device=DEV, dtype=torch.bfloat16)
+    w = torch.zeros((D, H // T), device=DEV, dtype=torch.bfloat16)
+    y = torch.empty((1, S, H // T), device=DEV, dtype=torch.bfloat16)
+    xr = torch.zeros((1, S, H // T), device=DEV, dtype=torch.bfloat16)
+    wr = torch.zeros((H // T, D), device=DEV, dtype=torch.bfloat16)
+    yr = torch.empty((1, S // T, D), device=DEV, dtype=torch.bfloat16)
+    q = torch.zeros((8, S, 128), device=DEV, dtype=torch.bfloat16)
+    o = torch.empty((1, S // T, T * 8 * 128), device=DEV, dtype=torch.bfloat16)
+    qs = torch.zeros((8 * T, S // T, 128), device=DEV, dtype=torch.bfloat16)
+    for _ in range(2):
+        comm.ag_gemm(x, w, y)
+        for kind in (tpf.RING, tpf.PAIRWISE, tpf.CIRCULAR):
+            comm.gemm_rs(xr, wr, yr, kind=kind)
+        comm.attention_a2a(q, q, q, o, 1, 8)
+        comm.ulysses_attention(qs, qs, qs, o, 1, 8 * T)
+    comm.sync()
+    comm.close()
