@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "tpf_internal.h"
 #include "tpf_ptx.cuh"
 
@@ -443,16 +445,23 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
 
 template <bool kQSplit>
 cudaError_t launch_fmha_instance(const FmhaParams& p, int grid, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, tpf_fmha_a2a_kernel<kQSplit>);
-    if (e != cudaSuccess) return e;
-    // the setmaxnreg split above must fit the pool the launch allocates, or the kernel hangs
-    if (fa.numRegs * 384 < 72 * 128 + 216 * 256) return cudaErrorInvalidConfiguration;
-    e = cudaFuncSetAttribute(tpf_fmha_a2a_kernel<kQSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
+  // function attributes are per device: set once per device, thread-safe
+  static std::mutex mu;
+  static uint64_t done = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!((done >> dev) & 1ull)) {
+      cudaFuncAttributes fa;
+      cudaError_t e = cudaFuncGetAttributes(&fa, tpf_fmha_a2a_kernel<kQSplit>);
+      if (e != cudaSuccess) return e;
+      // the setmaxnreg split above must fit the pool the launch allocates, or the kernel hangs
+      if (fa.numRegs * 384 < 72 * 128 + 216 * 256) return cudaErrorInvalidConfiguration;
+      e = cudaFuncSetAttribute(tpf_fmha_a2a_kernel<kQSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFSmem);
+      if (e != cudaSuccess) return e;
+      done |= 1ull << dev;
+    }
   }
   tpf_fmha_a2a_kernel<kQSplit><<<grid, 384, kFSmem, stream>>>(p);
   return cudaGetLastError();

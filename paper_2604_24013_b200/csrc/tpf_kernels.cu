@@ -31,6 +31,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+
 #include "tpf_internal.h"
 #include "tpf_ptx.cuh"
 
@@ -766,13 +768,25 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 
 namespace {
 
+// Function attributes are per device: set once per (instance, device), thread-safe.
+template <typename F>
+void once_per_device(uint64_t& done, F&& f) {
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (!((done >> dev) & 1ull)) {
+    f();
+    done |= 1ull << dev;
+  }
+}
+
 template <int kOp, int kMode>
 void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static uint64_t attr_done = 0;
+  once_per_device(attr_done, [] {
     cudaFuncSetAttribute(tpf_fused_kernel<kOp, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    attr_set = true;
-  }
+  });
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -810,8 +824,13 @@ void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
 // Largest number of co-resident CTA pairs (all CTAs must be resident: spins on
 // other CTAs' progress rely on it). All instances share block size and smem.
 int max_pairs() {
-  static int cached = -1;
-  if (cached >= 0) return cached;
+  static std::mutex mu;
+  static int cached[64];
+  static uint64_t have = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if ((have >> dev) & 1ull) return cached[dev];
   cudaFuncSetAttribute(tpf_fused_kernel<OP_RS, MODE_STD>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2);
@@ -826,7 +845,10 @@ int max_pairs() {
   cfg.numAttrs = 1;
   int n = 0;
   if (cudaOccupancyMaxActiveClusters(&n, tpf_fused_kernel<OP_RS, MODE_STD>, &cfg) != cudaSuccess) n = 0;
-  cached = n;
+  if (n > 0) {
+    cached[dev] = n;
+    have |= 1ull << dev;
+  }
   return n;
 }
 
