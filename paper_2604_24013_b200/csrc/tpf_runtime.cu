@@ -410,6 +410,10 @@ int hosted(const tpf_comm* c) { return c->local_group ? c->world : 1; }
 
 tpf::Status check_ready(const tpf_comm* c) {
   if (!c) return tpf::Status::invalid("null communicator");
+  int dev = -1;
+  if (cudaGetDevice(&dev) == cudaSuccess && dev != c->device)
+    return tpf::Status::invalid("communicator was created on device " + std::to_string(c->device) +
+                                " but the current device is " + std::to_string(dev));
   if (c->world > 1 && !c->peers_ready)
     return tpf::Status::invalid("communicator peers not opened (call tpf_comm_open_peers)");
   return tpf::Status::ok();
