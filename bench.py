@@ -356,6 +356,9 @@ def run_ours(args, rank, world, local_rank):
     emu = None
     if world == 1 and args.emulate_tp > 1:
         emu = emulated_block(args, dev, stream, args.emulate_tp)
+    virt = None
+    if world == 1 and args.emulate_tp > 1:
+        virt = virtual_block(args, dev, stream, args.emulate_tp)
 
     if rank != 0:
         return
@@ -418,7 +421,62 @@ def run_ours(args, rank, world, local_rank):
                                        "speedup_ours": base_ms / ms_step}
     if emu:
         out["emulated"] = emu
+    if virt:
+        out["virtual_per_gpu"] = virt
     print(json.dumps(out))
+
+
+def virtual_block(args, dev, stream, T):
+    """One GPU of a real TP=T group at full scale: rank 0 with virtual peers (every peer wait
+    passes at once, sends land in a scratch heap) runs the cfg2 block's per-rank AG-GEMM +
+    SwiGLU and GEMM-RS with the whole protocol. Against compute-only mode this is the
+    protocol's on-GPU cost per GPU; NVLink latency is the part it cannot show."""
+    import statistics
+
+    import torch
+
+    import paper_2604_24013_b200 as tpf
+    S_l, F_l = SEQ // T, FFN // T
+    g = torch.Generator(device=dev).manual_seed(11)
+    x = torch.randn((1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
+    w_gu = (torch.randn((D_MODEL, 2 * F_l), device=dev, generator=g) / 64).to(torch.bfloat16)
+    w_dn = (torch.randn((F_l, D_MODEL), device=dev, generator=g) / 120).to(torch.bfloat16)
+    act = torch.empty((1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
+                                                 tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
+
+    def timed(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        return e0.elapsed_time(e1)
+
+    ag = lambda: comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)  # noqa: E731
+    rs = lambda: comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)  # noqa: E731
+    for _ in range(3):
+        ag(); rs()
+    res = {"ag": [], "rs": [], "ag_co": [], "rs_co": []}
+    for _ in range(max(5, min(args.steps, 15))):
+        res["ag"].append(timed(ag))
+        res["rs"].append(timed(rs))
+        comm.set_compute_only(True)
+        res["ag_co"].append(timed(ag))
+        res["rs_co"].append(timed(rs))
+        comm.set_compute_only(False)
+    comm.sync(stream)
+    comm.close()
+    m = {k: statistics.median(v) for k, v in res.items()}
+    fl_ag, fl_rs = 2.0 * SEQ * D_MODEL * 2 * F_l, 2.0 * SEQ * F_l * D_MODEL
+    return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (waits pass at "
+                             "once, sends land in a local scratch heap); medians of single calls",
+            "ag_gemm_ms": m["ag"], "gemm_rs_ms": m["rs"], "compute_only_ag_ms": m["ag_co"],
+            "compute_only_rs_ms": m["rs_co"],
+            "ag_tflops_per_gpu": fl_ag / (m["ag"] * 1e-3) / 1e12, "rs_tflops_per_gpu": fl_rs / (m["rs"] * 1e-3) / 1e12,
+            "protocol_overhead_us": {"ag": 1e3 * (m["ag"] - m["ag_co"]), "rs": 1e3 * (m["rs"] - m["rs_co"])}}
 
 
 def emulated_block(args, dev, stream, T):
