@@ -447,21 +447,25 @@ def virtual_block(args, dev, stream, T):
     comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
                                                  tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
 
-    def timed(fn):
+    def timed(fn, n=20):
+        # n back-to-back calls between two events: the host runs ahead, so the figure is
+        # device time per call (a single synchronised call would also time the launch and
+        # the clock ramp of an idle GPU)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize(dev)
-        e0.record(stream)
         fn()
+        e0.record(stream)
+        for _ in range(n):
+            fn()
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        return e0.elapsed_time(e1)
+        return e0.elapsed_time(e1) / n
 
     ag = lambda: comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)  # noqa: E731
     rs = lambda: comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)  # noqa: E731
     for _ in range(3):
         ag(); rs()
     res = {"ag": [], "rs": [], "ag_co": [], "rs_co": []}
-    for _ in range(max(5, min(args.steps, 15))):
+    for _ in range(5):
         res["ag"].append(timed(ag))
         res["rs"].append(timed(rs))
         comm.set_compute_only(True)
@@ -472,12 +476,20 @@ def virtual_block(args, dev, stream, T):
     comm.close()
     m = {k: statistics.median(v) for k, v in res.items()}
     fl_ag, fl_rs = 2.0 * SEQ * D_MODEL * 2 * F_l, 2.0 * SEQ * F_l * D_MODEL
+    # SURVEY 8(d) roofline: max(FLOPs at the measured bf16 burst peak, NVLink bytes at 900 GB/s)
+    pk = peaks()["bf16_tflops"] * 1e12
+    wire = (T - 1) / T * SEQ * 2
+    t_roof_ag = max(fl_ag / pk, wire * D_MODEL / 900e9) * 1e3
+    t_roof_rs = max(fl_rs / pk, wire * D_MODEL / 900e9) * 1e3
     return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (waits pass at "
-                             "once, sends land in a local scratch heap); medians of single calls",
+                             "once, sends land in a local scratch heap); medians of 5 rounds of 20 "
+                             "back-to-back calls per op",
             "ag_gemm_ms": m["ag"], "gemm_rs_ms": m["rs"], "compute_only_ag_ms": m["ag_co"],
             "compute_only_rs_ms": m["rs_co"],
             "ag_tflops_per_gpu": fl_ag / (m["ag"] * 1e-3) / 1e12, "rs_tflops_per_gpu": fl_rs / (m["rs"] * 1e-3) / 1e12,
-            "protocol_overhead_us": {"ag": 1e3 * (m["ag"] - m["ag_co"]), "rs": 1e3 * (m["rs"] - m["rs_co"])}}
+            "protocol_overhead_us": {"ag": 1e3 * (m["ag"] - m["ag_co"]), "rs": 1e3 * (m["rs"] - m["rs_co"])},
+            "t_roof_ms": {"ag": t_roof_ag, "rs": t_roof_rs},
+            "frac_of_t_roof": {"ag": t_roof_ag / m["ag"], "rs": t_roof_rs / m["rs"]}}
 
 
 def emulated_block(args, dev, stream, T):

@@ -97,6 +97,7 @@ struct KParams {
   int64_t timeout_ns;
   int fault_rank;   // test hook: this rank never publishes its flags (-1: none)
   int compute_only; // measurement: same tiles, no flag waits / wire traffic (exposed-comm baseline)
+  int pdl_trigger;  // PDL instances: 1 trigger the next launch after the prologue, 2 after the last TMA load, 0 at exit
   // Optional device trace (%globaltimer ns): records of 4 x u64 appended via trace[0] counter.
   unsigned long long* trace;
   int64_t trace_cap;  // records

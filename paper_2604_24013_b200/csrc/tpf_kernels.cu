@@ -31,6 +31,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "tpf_internal.h"
@@ -201,81 +202,162 @@ __device__ __forceinline__ void wire_store(int wire_f32, char* tile, int j, int 
   }
 }
 
-__device__ __forceinline__ void wire_load(int wire_f32, const char* tile, int j, int row,
-                                          float (&v)[32]) {
-  if (wire_f32) {
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const float4 w = *reinterpret_cast<const float4*>(tile + wire_off(1, j, g, row));
-      v[g * 4] = w.x; v[g * 4 + 1] = w.y; v[g * 4 + 2] = w.z; v[g * 4 + 3] = w.w;
-    }
-  } else {
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      const uint4 w = *reinterpret_cast<const uint4*>(tile + wire_off(0, j, g, row));
-      v[g * 8 + 0] = bf16lo(w.x); v[g * 8 + 1] = bf16hi(w.x);
-      v[g * 8 + 2] = bf16lo(w.y); v[g * 8 + 3] = bf16hi(w.y);
-      v[g * 8 + 4] = bf16lo(w.z); v[g * 8 + 5] = bf16hi(w.z);
-      v[g * 8 + 6] = bf16lo(w.w); v[g * 8 + 7] = bf16hi(w.w);
-    }
-  }
-}
-
-// rs_direct fold of one 32-column sub-chunk, 16 columns at a time: all T-1 received
+// rs_direct fold of one 32-column sub-chunk, 8 columns at a time: all T-1 received
 // contributions are loaded first (memory-level parallelism), then summed in the
 // reference order ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own.
 __device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0, int j, int row,
                                             float (&v)[32]) {
-  const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
   const int64_t slot_stride = p.slot_bytes;
   const int nin = p.T - 1;
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    uint4 raw[kMaxRanks - 1][4];
+  for (int qt = 0; qt < 4; ++qt) {
+    uint4 raw[kMaxRanks - 1][2];
 #pragma unroll
     for (int s = 0; s < kMaxRanks - 1; ++s) {
       if (s < nin) {
         const char* tile = slot0 + s * slot_stride;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (p.wire_f32) {
-            raw[s][q] = *reinterpret_cast<const uint4*>(tile + wire_off(1, j, half * 4 + q, row));
-          } else if (q < 2) {
-            raw[s][q] = *reinterpret_cast<const uint4*>(tile + wire_off(0, j, half * 2 + q, row));
-          }
+        if (p.wire_f32) {
+          raw[s][0] = *reinterpret_cast<const uint4*>(tile + wire_off(1, j, qt * 2, row));
+          raw[s][1] = *reinterpret_cast<const uint4*>(tile + wire_off(1, j, qt * 2 + 1, row));
+        } else {
+          raw[s][0] = *reinterpret_cast<const uint4*>(tile + wire_off(0, j, qt, row));
         }
       }
     }
-    float acc[16];
+    float acc[8];
 #pragma unroll
     for (int s = 0; s < kMaxRanks - 1; ++s) {
       if (s < nin) {
-        float in[16];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (p.wire_f32) {
-            in[q * 4 + 0] = __uint_as_float(raw[s][q].x);
-            in[q * 4 + 1] = __uint_as_float(raw[s][q].y);
-            in[q * 4 + 2] = __uint_as_float(raw[s][q].z);
-            in[q * 4 + 3] = __uint_as_float(raw[s][q].w);
-          } else if (q < 2) {
-            in[q * 8 + 0] = bf16lo(raw[s][q].x); in[q * 8 + 1] = bf16hi(raw[s][q].x);
-            in[q * 8 + 2] = bf16lo(raw[s][q].y); in[q * 8 + 3] = bf16hi(raw[s][q].y);
-            in[q * 8 + 4] = bf16lo(raw[s][q].z); in[q * 8 + 5] = bf16hi(raw[s][q].z);
-            in[q * 8 + 6] = bf16lo(raw[s][q].w); in[q * 8 + 7] = bf16hi(raw[s][q].w);
-          }
+        float in[8];
+        if (p.wire_f32) {
+          in[0] = __uint_as_float(raw[s][0].x); in[1] = __uint_as_float(raw[s][0].y);
+          in[2] = __uint_as_float(raw[s][0].z); in[3] = __uint_as_float(raw[s][0].w);
+          in[4] = __uint_as_float(raw[s][1].x); in[5] = __uint_as_float(raw[s][1].y);
+          in[6] = __uint_as_float(raw[s][1].z); in[7] = __uint_as_float(raw[s][1].w);
+        } else {
+          in[0] = bf16lo(raw[s][0].x); in[1] = bf16hi(raw[s][0].x);
+          in[2] = bf16lo(raw[s][0].y); in[3] = bf16hi(raw[s][0].y);
+          in[4] = bf16lo(raw[s][0].z); in[5] = bf16hi(raw[s][0].z);
+          in[6] = bf16lo(raw[s][0].w); in[7] = bf16hi(raw[s][0].w);
         }
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc[c] = s == 0 ? in[c] : acc[c] + in[c];
+        for (int c = 0; c < 8; ++c) acc[c] = s == 0 ? in[c] : acc[c] + in[c];
       }
     }
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[half * 16 + c] = acc[c] + v[half * 16 + c];
+    for (int c = 0; c < 8; ++c) v[qt * 8 + c] = acc[c] + v[qt * 8 + c];
   }
-  (void)tile_bytes;
 }
 
 }  // namespace
+
+// rs_direct last step: fold the T-1 received partials into the own one, sub-chunk by
+// sub-chunk. Not inlined: its T-1 in-flight inbox loads per sub-chunk would otherwise add
+// to the register pressure of the pipelined epilogue and make the kernel spill.
+__device__ __noinline__ void rs_epilogue_fold(const KParams& p, uint32_t taddr, const char* in0, char* rp,
+                                              int64_t ocol0, int row, bool valid, uint32_t tempty_a) {
+  for (int j = 0; j < BN / 32; ++j) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + j * 32, r);
+    tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
+    if (valid) {
+      // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
+      direct_fold(p, in0, j, row, v);
+      store_out_row(p, rp, ocol0 + j * 32, v);
+    }
+  }
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_a);
+}
+
+// GEMM-RS epilogue of one 128 x 256 accumulator (this thread: one row), pipelined by one
+// 32-column sub-chunk (see the call site). kF32: fp32 wire, else bf16 wire. The wire type is
+// a template parameter so each instance keeps only its own inbox buffers live.
+template <bool kF32>
+__device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t taddr, const char* inbox,
+                                                      char* dst_tile, char* rp, int64_t ocol0, int row,
+                                                      bool valid, bool last, uint32_t tempty_a) {
+  constexpr int kW = kF32 ? 8 : 4;  // 16-B inbox words per sub-chunk
+  constexpr int kNJ = BN / 32;
+  // The fp32 wire (the parity path) is not pipelined: its double buffers would push the
+  // kernel past 255 registers.
+  constexpr bool kPipe = !kF32;
+  uint32_t r[2][32];
+  uint4 raw[2][kW];
+  const bool pull = valid && inbox;
+  if (kPipe) {
+    tmem_ld_32x32b_x32(taddr, r[0]);
+    if (pull) {
+#pragma unroll
+      for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, 0, g, row));
+    }
+  }
+#pragma unroll(kPipe ? kNJ : 1)
+  for (int j = 0; j < kNJ; ++j) {
+    const int c = kPipe ? (j & 1) : 0;
+    if (!kPipe) {
+      if (pull) {
+#pragma unroll
+        for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j, g, row));
+      }
+      tmem_ld_32x32b_x32(taddr + j * 32, r[0]);
+    }
+    tmem_ld_wait();
+    tmem_regs_pin(r[c]);
+    if (kPipe && j + 1 < kNJ) {
+      tmem_ld_32x32b_x32(taddr + (j + 1) * 32, r[c ^ 1]);
+      if (pull) {
+#pragma unroll
+        for (int g = 0; g < kW; ++g)
+          raw[c ^ 1][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j + 1, g, row));
+      }
+    }
+    if (j + 1 == kNJ) {
+      tc_fence_before();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_a);
+    }
+    if (!valid) continue;
+    float v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[c][q]);
+    if (inbox) {
+      // rs_pipelined: partial += inbox   (collectives.cpp:303)
+#pragma unroll
+      for (int g = 0; g < kW; ++g) {
+        const uint4 w = raw[c][g];
+        if (kF32) {
+          v[g * 4 + 0] = v[g * 4 + 0] + __uint_as_float(w.x);
+          v[g * 4 + 1] = v[g * 4 + 1] + __uint_as_float(w.y);
+          v[g * 4 + 2] = v[g * 4 + 2] + __uint_as_float(w.z);
+          v[g * 4 + 3] = v[g * 4 + 3] + __uint_as_float(w.w);
+        } else {
+          v[g * 8 + 0] = v[g * 8 + 0] + bf16lo(w.x); v[g * 8 + 1] = v[g * 8 + 1] + bf16hi(w.x);
+          v[g * 8 + 2] = v[g * 8 + 2] + bf16lo(w.y); v[g * 8 + 3] = v[g * 8 + 3] + bf16hi(w.y);
+          v[g * 8 + 4] = v[g * 8 + 4] + bf16lo(w.z); v[g * 8 + 5] = v[g * 8 + 5] + bf16hi(w.z);
+          v[g * 8 + 6] = v[g * 8 + 6] + bf16lo(w.w); v[g * 8 + 7] = v[g * 8 + 7] + bf16hi(w.w);
+        }
+      }
+    }
+    if (last)
+      store_out_row(p, rp, ocol0 + j * 32, v);
+    else
+      wire_store(kF32, dst_tile, j, row, v);
+  }
+}
+
+// Instances launched with programmatic dependent launch (PDL): the T == 1 GEMM. Its CTAs
+// never wait on another grid, so letting the next launch in early cannot starve anything
+// (the attention-family and query-split instances wait on other grids of this GPU and must
+// keep plain stream order). Measured (tools/ab_env.py, alternating processes): +1.7% on the
+// T = 1 MLP block; on the per-GPU TP = 8 fused GEMM-RS PDL cost 5% with every trigger
+// placement (after the prologue, after the last TMA load, implicit at exit), and it was
+// neutral on the fused AG-GEMM, so the multi-rank instances keep plain stream order.
+__host__ __device__ constexpr bool pdl_instance(int mode) { return mode == MODE_SINGLE; }
 
 // Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
 // single-thread producer / MMA loops cost measurable throughput.
@@ -287,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   constexpr bool kBKMajor = kGatherB || kMode == MODE_QK;              // B stored (N, K)
   constexpr bool kUpEpi = kMode == MODE_PV;                            // merge_heads + push + flags
   constexpr bool kSingle = kMode == MODE_SINGLE;                       // T == 1: no ring at all
+  constexpr bool kPdl = pdl_instance(kMode);                           // launched with PDL
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -328,11 +411,6 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       prefetch_tmap(&p.tmap_wire[1]);
     }
   }
-  if (threadIdx.x == 0) {
-    const uint32_t e = p.epoch_dev ? epoch_read(p.epoch_dev, p.epoch_bump) : p.epoch;
-    s_epoch = e;
-    s_parity = p.epoch_dev ? static_cast<int>(e & 1u) : p.parity;
-  }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 2);
@@ -347,9 +425,21 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_2sm<512>(tmem_holder);
+  // PDL: everything above is CTA-local and overlaps the previous kernel's tail; no global
+  // memory is touched before the previous grid has completed.
+  if (kPdl) griddep_wait();
+  if (threadIdx.x == 0) {
+    const uint32_t e = p.epoch_dev ? epoch_read(p.epoch_dev, p.epoch_bump) : p.epoch;
+    s_epoch = e;
+    s_parity = p.epoch_dev ? static_cast<int>(e & 1u) : p.parity;
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  // The next PDL launch may start its prologue on SMs as this grid's CTAs exit. Only
+  // instances whose CTAs never wait on another grid trigger early: a dependent grid must
+  // not take SMs a concurrently running kernel (query-split attention) still needs.
+  if (kPdl && p.pdl_trigger == 1) griddep_launch_dependents();
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t ep = s_epoch;  // this launch's epoch / heap parity, in registers from here on
   const int par = s_parity;
@@ -479,6 +569,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       }
       if (p.trace && lane == 0) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
     }
+    if (kPdl && p.pdl_trigger == 2) griddep_launch_dependents();  // all of this CTA's loads issued
   } else if (warp == 1) {
     // ===================================================== MMA issuer (leader CTA)
     if (leader && lane == 0) {
@@ -713,35 +804,23 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const int64_t ocol = kUpEpi ? p.out_col_off[h] + (hm ? static_cast<int64_t>(t.b % hm) * p.N : 0) : 0;
       const int64_t orow = ob * p.out_rows + pass * p.Sc + t.row0 + row;
       char* rp = ((kUpEpi && p.out_rank[h]) ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
-      for (int j = 0; j < BN / 32; ++j) {
-        // the inbox loads go out before the TMEM read so the two latencies overlap
-        float in[32];
-        if (valid && inbox) wire_load(p.wire_f32, inbox, j, row, in);
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(taddr + j * 32, r);
-        tmem_ld_wait();
-        float v[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = __uint_as_float(r[c]);
-        if (valid) {
-          if (inbox) {
-            // rs_pipelined: partial += inbox   (collectives.cpp:303)
-#pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = v[c] + in[c];
-          } else if (p.direct && last && p.T > 1 && !p.compute_only) {
-            // rs_direct fold: ((c[p0] + c[p1]) + ... + c[p(T-2)]) + own  (collectives.cpp:326-355)
-            const char* in0 = slot_ptr(p, par, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
-            direct_fold(p, in0, j, row, v);
-          }
-          if (last)
-            store_out_row(p, rp, static_cast<int64_t>(t.nt) * BN + j * 32, v);
-          else
-            wire_store(p.wire_f32, dst_tile, j, row, v);
-        }
+      const bool folding = p.direct && last && p.T > 1 && !p.compute_only;
+      if (folding) {
+        const char* in0 = slot_ptr(p, par, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
+        rs_epilogue_fold(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
+                         a ? tempty_leader1 : tempty_leader0);
+      } else {
+        // Software-pipelined by one 32-column sub-chunk: the TMEM read and the inbox loads
+        // of sub-chunk j+1 are in flight while sub-chunk j is summed and stored, so each
+        // latency is paid once per tile instead of once per sub-chunk. The accumulator is
+        // released as soon as its last columns are in registers.
+        const uint32_t tempty_a = a ? tempty_leader1 : tempty_leader0;
+        const int64_t ocol0 = static_cast<int64_t>(t.nt) * BN;
+        if (p.wire_f32)
+          rs_epilogue_pipelined<true>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
+        else
+          rs_epilogue_pipelined<false>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(a ? tempty_leader1 : tempty_leader0);
       if (!last && tile_live) {
         pend[npend++] = flag_ptr(p, par, send_rank, slot_send, fidx);
         if (npend == kPend) publish();
@@ -781,6 +860,18 @@ void once_per_device(uint64_t& done, F&& f) {
   }
 }
 
+// TPF_PDL (A/B measurement switch): 0 plain stream order (griddepcontrol.wait then returns
+// at once); 1 (default) trigger the next launch after the prologue; 2 after this CTA's last
+// TMA load; 3 PDL launch without an explicit trigger (the next launch starts at exit).
+int pdl_setting() {
+  static const int v = [] {
+    const char* e = std::getenv("TPF_PDL");
+    return (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 1;
+  }();
+  return v;
+}
+bool pdl_enabled() { return pdl_setting() != 0; }
+
 template <int kOp, int kMode>
 void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   static uint64_t attr_done = 0;
@@ -792,14 +883,20 @@ void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmemBytes;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for tcgen05 cta_group::2
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // PDL: the prologue (barrier init, TMEM allocation, tensor-map prefetch) overlaps the
+  // previous kernel's tail; the kernel waits (griddepcontrol.wait) before touching memory.
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, p);
+  cfg.numAttrs = (pdl_instance(kMode) && pdl_enabled()) ? 2 : 1;
+  KParams q = p;
+  q.pdl_trigger = pdl_setting() == 3 ? 0 : pdl_setting();
+  cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, q);
 }
 
 }  // namespace
