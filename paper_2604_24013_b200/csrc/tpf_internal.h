@@ -12,7 +12,11 @@ constexpr int BM = 128;          // rows per CTA; the CTA pair computes 256 x BN
 constexpr int BN = 256;          // UMMA N (each CTA of the pair stages BN/2 columns of B)
 constexpr int BK = 64;           // 64 bf16 = one 128 B swizzle atom row
 constexpr int kStages = 6;
-constexpr int kThreads = 256;    // 8 warps: TMA, MMA, 2x comm, 4x epilogue
+constexpr int kThreads = 384;    // 12 warps: TMA, MMA, 2x comm, 2 x 4 epilogue (one group per accumulator)
+constexpr int kRegPool = 168;    // registers per thread the launch allocates (__launch_bounds__(384, 1))
+constexpr int kRegsCtl = 80;     // setmaxnreg: warps 0-3 (the AG forwarders spill below 80)
+constexpr int kRegsEpi = 208;    // setmaxnreg: epilogue warpgroups (128 * 80 + 256 * 208 <= 384 * 168)
+static_assert(128 * kRegsCtl + 256 * kRegsEpi <= kThreads * kRegPool, "setmaxnreg split exceeds the pool");
 constexpr int kAStageBytes = BM * BK * 2;        // 16 KiB: also the AG wire "image" unit
 constexpr int kBStageBytes = (BN / 2) * BK * 2;  // 16 KiB: this CTA's half of B
 constexpr int kStageBytes = kAStageBytes + kBStageBytes;
@@ -112,6 +116,8 @@ enum TraceKind : int {
   TR_WAIT_IN = 5,    // index = tile lin; epilogue blocked on an RS inbox flag
   TR_FLAG = 6,       // index = tile lin; RS flag published to the successor at t1
   TR_FLUSH = 7,      // index = #flags; AG forwarder fence + flag publication (t1-t0)
+  TR_EPI_LOOP = 8,   // index = tile lin; RS epilogue: t0 = accumulator ready, t1 = stores issued
+  TR_PUBLISH = 9,    // index = #flags; RS epilogue system fence + flag publication (t1-t0)
 };
 
 // UP v2: fused flash-attention + output all-to-all (csrc/tpf_attention.cu)
@@ -151,7 +157,7 @@ struct UlyssesParams {
 };
 
 void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream);
-void launch_fused(const KParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
 // Wait until flags[parity][0..n) >= epoch, epoch / parity read from epoch_dev (the call's

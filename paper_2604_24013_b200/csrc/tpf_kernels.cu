@@ -275,47 +275,39 @@ __device__ __noinline__ void rs_epilogue_fold(const KParams& p, uint32_t taddr, 
 }
 
 // GEMM-RS epilogue of one 128 x 256 accumulator (this thread: one row), pipelined by one
-// 32-column sub-chunk (see the call site). kF32: fp32 wire, else bf16 wire. The wire type is
-// a template parameter so each instance keeps only its own inbox buffers live.
+// 32-column sub-chunk: the inbox loads of sub-chunk j+1 are in flight while sub-chunk j is
+// read from TMEM, summed and stored (bf16 wire; the fp32 parity wire loads its inbox in
+// the same iteration). The accumulator is released as soon as its last columns are in
+// registers. kF32 is a template parameter so each instance keeps only its own buffers live.
 template <bool kF32>
 __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t taddr, const char* inbox,
                                                       char* dst_tile, char* rp, int64_t ocol0, int row,
                                                       bool valid, bool last, uint32_t tempty_a) {
   constexpr int kW = kF32 ? 8 : 4;  // 16-B inbox words per sub-chunk
   constexpr int kNJ = BN / 32;
-  // The fp32 wire (the parity path) is not pipelined: its double buffers would push the
-  // kernel past 255 registers.
-  constexpr bool kPipe = !kF32;
-  uint32_t r[2][32];
+  constexpr bool kAhead = !kF32;
+  uint32_t r[32];
   uint4 raw[2][kW];
   const bool pull = valid && inbox;
-  if (kPipe) {
-    tmem_ld_32x32b_x32(taddr, r[0]);
-    if (pull) {
+  if (pull && kAhead) {
 #pragma unroll
-      for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, 0, g, row));
-    }
+    for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, 0, g, row));
   }
-#pragma unroll(kPipe ? kNJ : 1)
+#pragma unroll(kAhead ? kNJ : 1)
   for (int j = 0; j < kNJ; ++j) {
-    const int c = kPipe ? (j & 1) : 0;
-    if (!kPipe) {
-      if (pull) {
+    const int c = kAhead ? (j & 1) : 0;
+    if (pull) {
+      if (!kAhead) {
 #pragma unroll
         for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j, g, row));
-      }
-      tmem_ld_32x32b_x32(taddr + j * 32, r[0]);
-    }
-    tmem_ld_wait();
-    tmem_regs_pin(r[c]);
-    if (kPipe && j + 1 < kNJ) {
-      tmem_ld_32x32b_x32(taddr + (j + 1) * 32, r[c ^ 1]);
-      if (pull) {
+      } else if (j + 1 < kNJ) {
 #pragma unroll
         for (int g = 0; g < kW; ++g)
           raw[c ^ 1][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j + 1, g, row));
       }
     }
+    tmem_ld_32x32b_x32(taddr + j * 32, r);
+    tmem_ld_wait();
     if (j + 1 == kNJ) {
       tc_fence_before();
       __syncwarp();
@@ -324,7 +316,7 @@ __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t
     if (!valid) continue;
     float v[32];
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[c][q]);
+    for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
     if (inbox) {
       // rs_pipelined: partial += inbox   (collectives.cpp:303)
 #pragma unroll
@@ -446,253 +438,266 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   const CUtensorMap* wmap = &p.tmap_wire[par];
 
   if (!active) {
-  } else if (warp == 0) {
-    // ===================================================== TMA producer (both CTAs)
-    // With AG wire inputs the whole warp walks the schedule (the wire-image flag scan is
-    // warp-parallel); otherwise lane 0 alone. Lane 0 issues barrier arrivals and TMA loads.
-    const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
-      const Tile t = get_tile(p, lin, cta);
-      const int pass = t.step / p.T, it = t.step - pass * p.T;
-      const bool from_wire = !kSingle && (kOp == OP_AG) && it > 0 && !p.compute_only;
-      const bool a_from_wire = from_wire && !kGatherB;
-      const bool b_from_wire = from_wire && kGatherB;
-      int64_t arow;
-      if (t.valid == 0)
-        arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
-      else if (kOp == OP_RS)
-        arow = (kMode == MODE_QK ? p.a_row_off[h] : 0) +
-               (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
-      else if (kGatherB)
-        arow = t.row0;
-      else
-        arow = pass * p.Sc + t.row0;
-      const int aslot = pass * (p.T - 1) + it - 1;
-      // wire images of this CTA's operand for this tile: A rows (m-block) or B half (n-tile)
-      const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
-                                      : static_cast<int64_t>(t.mb) * p.nkb;
-      const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
-      const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
-      int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
-      uint64_t t_first = 0;
-      const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
-      const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
-      if (kMode == MODE_QSPLIT && t.valid > 0 && lane == 0 && !p.compute_only) {
-        // the A rows of this step's query slice come from the concurrently running attention
-        // kernel (generic stores): wait for the slice's counter, then order the TMA reads
-        const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
-        const uint32_t* cnt = p.qs_ready[h] + l;
-        if (ld_acquire_gpu(cnt) < p.qs_target) {
-          const uint64_t tq0 = globaltimer();
-          while (ld_acquire_gpu(cnt) < p.qs_target) {
-            if (aborted(p)) break;
-            if (globaltimer() - tq0 > static_cast<uint64_t>(p.timeout_ns)) {
-              record_error(p, 1, rank, t.step, lin);
-              break;
-            }
-            __nanosleep(256);
-          }
-        }
-        fence_proxy_async_global();
-      }
-      for (int kb = 0; kb < p.nkb; ++kb) {
-        if (wire_live && kb > ready) {
-          // Wait for image kb, then claim the run of consecutive landed images: every lane
-          // acquire-loads one flag (system scope), the warp barrier carries that ordering to
-          // lane 0, whose proxy fence orders it before the TMA (async-proxy) reads.
-          const uint64_t tw0 = p.trace ? globaltimer() : 0;
-          if (lane == 0) wait_flag(p, mflags + kb, rank, t.step, lin, ep);
-          __syncwarp();
-          ready = kb;
-          while (ready + 1 < p.nkb) {
-            const int k = ready + 1 + lane;
-            const bool ok = k >= p.nkb || ld_acquire_sys(mflags + k) >= ep;
-            const uint32_t m = __ballot_sync(0xffffffffu, ok);
-            const int run = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
-            ready = min(ready + run, p.nkb - 1);
-            if (run < 32) break;
-          }
-          __syncwarp();
-          if (lane == 0) fence_proxy_async_global();
-          if (p.trace && lane == 0) {
-            const uint64_t tw1 = globaltimer();
-            if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
-          }
-        }
-        if (lane == 0) {
-          mbar_wait(p, empty + stage, phase ^ 1);
-          // Stages the forwarder will not touch: arrive on its behalf (empty counts 2).
-          if (fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
-          uint8_t* sa = smem_a + stage * kAStageBytes;
-          uint8_t* sb = smem_b + stage * kBStageBytes;
-          const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
-          const int img = static_cast<int>(img0) + kb;
-          if (leader)
-            mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
-          else
-            mbar_arrive_cluster(fb);
-          if (a_from_wire) {
-            tma_load_2sm_5d(sa, wmap, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
-          } else if (kAMn) {
-            // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
-#pragma unroll
-            for (int q = 0; q < BM / 64; ++q)
-              tma_load_2sm_4d(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
-                              t.b, h);
-          } else {
-            tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
-          }
-          if (b_from_wire) {
-            tma_load_2sm_5d(sb, wmap, fb, 0, 0, img, aslot, h);
-          } else if (kBKMajor) {
-            // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
-            if (kBBatched)
-              tma_load_2sm_4d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
-            else
-              tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
-          } else {
-#pragma unroll
-            for (int q = 0; q < BN / 128; ++q) {
-              if (kBBatched)
-                tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
-                                kb * BK, t.b, h);
-              else
-                tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
-                                kb * BK, h);
-            }
-          }
-          if (p.trace && kb == 0) t_first = globaltimer();
-        }
-        if (++stage == kStages) { stage = 0; phase ^= 1; }
-      }
-      if (p.trace && lane == 0) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
-    }
-    if (kPdl && p.pdl_trigger == 2) griddep_launch_dependents();  // all of this CTA's loads issued
-  } else if (warp == 1) {
-    // ===================================================== MMA issuer (leader CTA)
-    if (leader && lane == 0) {
-      const uint32_t idesc =
-          make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/!kBKMajor, /*a_mn_major=*/kAMn);
+  } else if (warp < 4) {
+    // Register split (384 threads, pool kRegPool per thread at launch): warps 0-3 (TMA,
+    // MMA, TMEM / forwarders) need few; the two epilogue warpgroups hold a 32-column
+    // TMEM chunk pipeline each. setmaxnreg.inc blocks until the pool can satisfy it, so
+    // the split must fit the pool the launch allocates (checked in launch_instance).
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+    if (warp == 0) {
+      // ===================================================== TMA producer (both CTAs)
+      // With AG wire inputs the whole warp walks the schedule (the wire-image flag scan is
+      // warp-parallel); otherwise lane 0 alone. Lane 0 issues barrier arrivals and TMA loads.
+      const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
       int stage = 0;
       uint32_t phase = 0;
-      int lt = 0;
-      int fo = 0;  // ordinal of forwarded stage uses (same sequence in all roles)
-      for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
-        const int a = lt & 1;
-        const uint32_t use = static_cast<uint32_t>(lt >> 1);
-        mbar_wait(p, tempty + a, (use & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem_base + a * BN;
-        int fwd_nt = -1;
-        if (fwd) {
-          const Tile t = get_tile(p, lin, 0);
-          const int it = t.step % p.T;
-          const int key = kGatherB ? t.pair : t.nt;
-          if (it < p.T - 1 && key < nfwd) fwd_nt = key;
-        }
-        for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait(p, full + stage, phase);
-          tc_fence_after();
-          if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
-            uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kStages + stage;
-            mbar_arrive(fr);
-            mbar_arrive_cluster(mapa_shared(smem_u32(fr), 1));
-            ++fo;
-          }
-          const uint32_t abase = smem_u32(smem_a + stage * kAStageBytes);
-          const uint32_t bbase = smem_u32(smem_b + stage * kBStageBytes);
-#pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
-            // MN-major A: like B, 16 K-rows = 2048 B, LBO = 64-row atom (8 KiB), SBO = 1 KiB.
-            const uint64_t ad = kAMn ? make_sdesc(abase + k * 2048, 64 * BK * 2, 1024)
-                                       : make_sdesc(abase + k * 32, 0, 1024);
-            // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
-            // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
-            const uint64_t bd = kBKMajor ? make_sdesc(bbase + k * 32, 0, 1024)
-                                                           : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
-            mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          mma_commit_2sm(empty + stage, 0x3);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
-        }
-        mma_commit_2sm(tfull + a, 0x3);
-      }
-    }
-  } else if (warp == 2 || warp == 3) {
-    // ===================================================== AG ring forwarders (warps 2-3)
-    // Forwarded stage uses (tile nt < nfwd, k-block kb % nfwd == nt) are split into batches
-    // of fbatch alternating between the two warps. For each of its uses a warp waits on its
-    // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B A image out of SMEM
-    // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4 into
-    // the successor's slot (NVLink peer stores). At the end of its batch (and of every tile)
-    // the warp fences its stores at system scope and publishes the image flags; while one
-    // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
-    // which keeps the ring's progress argument (step-i images depend only on step i-1).
-    if (fwd) {
-      const int grp = warp - 2;
-      uint32_t* unpub[16];
-      int nunpub = 0;
-      uint32_t ph = 0;  // per-stage phase bits of this group's fwd_ready barriers
-      int fo = 0;
-      auto flush = [&]() {
-        const uint64_t tf0 = p.trace ? globaltimer() : 0;
-        fence_sys();
-        __syncwarp();
-        if (lane == 0 && rank != p.fault_rank)
-          for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], ep);
-        if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
-        nunpub = 0;
-      };
-      int lt = 0;
-      for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+      for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
-        const int key = kGatherB ? t.pair : t.nt;
-        if (!(it < p.T - 1 && key < nfwd)) continue;
-        const int slot = pass * (p.T - 1) + it;
-        const int dst_rank = p.sched[rank][it][0];
-        const uint64_t t0 = p.trace ? globaltimer() : 0;
-        // forwarded operand: this CTA's A rows, or (gather_b) its half of the B tile
-        const bool live = kGatherB ? true : t.valid > 0;
+        const bool from_wire = !kSingle && (kOp == OP_AG) && it > 0 && !p.compute_only;
+        const bool a_from_wire = from_wire && !kGatherB;
+        const bool b_from_wire = from_wire && kGatherB;
+        int64_t arow;
+        if (t.valid == 0)
+          arow = p.x_rows;  // whole box out of bounds: TMA zero-fills, bytes still counted
+        else if (kOp == OP_RS)
+          arow = (kMode == MODE_QK ? p.a_row_off[h] : 0) +
+                 (p.T > 1 ? (static_cast<int64_t>(p.sched[rank][it][2]) * p.m + pass) : 0) * p.Sc + t.row0;
+        else if (kGatherB)
+          arow = t.row0;
+        else
+          arow = pass * p.Sc + t.row0;
+        const int aslot = pass * (p.T - 1) + it - 1;
+        // wire images of this CTA's operand for this tile: A rows (m-block) or B half (n-tile)
         const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
                                         : static_cast<int64_t>(t.mb) * p.nkb;
-        const uint8_t* sbase = kGatherB ? smem_b : smem_a;
-        for (int kb = key; kb < p.nkb; kb += nfwd) {
-          const bool mine = ((fo / fbatch) & 1) == grp;
-          const bool batch_end = (fo % fbatch) == fbatch - 1;
-          ++fo;
-          if (!mine) continue;
-          const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kStages);
-          mbar_wait(p, fwd_ready + grp * kStages + stage, (ph >> stage) & 1u);
-          ph ^= 1u << stage;
-          if (live) {
-            const int64_t img = img0 + kb;
-            const uint4* src = reinterpret_cast<const uint4*>(sbase + stage * kAStageBytes);
-            uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes);
-#pragma unroll
-            for (int half = 0; half < 2; ++half) {
-              uint4 v[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] = src[(half * 16 + i) * 32 + lane];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) dst[(half * 16 + i) * 32 + lane] = v[i];
+        const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
+        const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
+        int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
+        uint64_t t_first = 0;
+        const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
+        const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
+        if (kMode == MODE_QSPLIT && t.valid > 0 && lane == 0 && !p.compute_only) {
+          // the A rows of this step's query slice come from the concurrently running attention
+          // kernel (generic stores): wait for the slice's counter, then order the TMA reads
+          const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
+          const uint32_t* cnt = p.qs_ready[h] + l;
+          if (ld_acquire_gpu(cnt) < p.qs_target) {
+            const uint64_t tq0 = globaltimer();
+            while (ld_acquire_gpu(cnt) < p.qs_target) {
+              if (aborted(p)) break;
+              if (globaltimer() - tq0 > static_cast<uint64_t>(p.timeout_ns)) {
+                record_error(p, 1, rank, t.step, lin);
+                break;
+              }
+              __nanosleep(256);
             }
-            unpub[nunpub++] = flag_ptr(p, par, dst_rank, slot, img);
           }
-          __syncwarp();  // every lane's SMEM reads of the stage are done
-          if (lane == 0) mbar_arrive(empty + stage);
-          if (batch_end && nunpub > 0) flush();
+          fence_proxy_async_global();
         }
-        if (nunpub > 0) flush();
-        if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          if (wire_live && kb > ready) {
+            // Wait for image kb, then claim the run of consecutive landed images: every lane
+            // acquire-loads one flag (system scope), the warp barrier carries that ordering to
+            // lane 0, whose proxy fence orders it before the TMA (async-proxy) reads.
+            const uint64_t tw0 = p.trace ? globaltimer() : 0;
+            if (lane == 0) wait_flag(p, mflags + kb, rank, t.step, lin, ep);
+            __syncwarp();
+            ready = kb;
+            while (ready + 1 < p.nkb) {
+              const int k = ready + 1 + lane;
+              const bool ok = k >= p.nkb || ld_acquire_sys(mflags + k) >= ep;
+              const uint32_t m = __ballot_sync(0xffffffffu, ok);
+              const int run = (m == 0xffffffffu) ? 32 : __ffs(~m) - 1;
+              ready = min(ready + run, p.nkb - 1);
+              if (run < 32) break;
+            }
+            __syncwarp();
+            if (lane == 0) fence_proxy_async_global();
+            if (p.trace && lane == 0) {
+              const uint64_t tw1 = globaltimer();
+              if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
+            }
+          }
+          if (lane == 0) {
+            mbar_wait(p, empty + stage, phase ^ 1);
+            // Stages the forwarder will not touch: arrive on its behalf (empty counts 2).
+            if (fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
+            uint8_t* sa = smem_a + stage * kAStageBytes;
+            uint8_t* sb = smem_b + stage * kBStageBytes;
+            const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
+            const int img = static_cast<int>(img0) + kb;
+            if (leader)
+              mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
+            else
+              mbar_arrive_cluster(fb);
+            if (a_from_wire) {
+              tma_load_2sm_5d(sa, wmap, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
+            } else if (kAMn) {
+              // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
+  #pragma unroll
+              for (int q = 0; q < BM / 64; ++q)
+                tma_load_2sm_4d(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
+                                t.b, h);
+            } else {
+              tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
+            }
+            if (b_from_wire) {
+              tma_load_2sm_5d(sb, wmap, fb, 0, 0, img, aslot, h);
+            } else if (kBKMajor) {
+              // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
+              if (kBBatched)
+                tma_load_2sm_4d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
+              else
+                tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
+            } else {
+  #pragma unroll
+              for (int q = 0; q < BN / 128; ++q) {
+                if (kBBatched)
+                  tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                                  kb * BK, t.b, h);
+                else
+                  tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                                  kb * BK, h);
+              }
+            }
+            if (p.trace && kb == 0) t_first = globaltimer();
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        if (p.trace && lane == 0) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
+      }
+      if (kPdl && p.pdl_trigger == 2) griddep_launch_dependents();  // all of this CTA's loads issued
+    } else if (warp == 1) {
+      // ===================================================== MMA issuer (leader CTA)
+      if (leader && lane == 0) {
+        const uint32_t idesc =
+            make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/!kBKMajor, /*a_mn_major=*/kAMn);
+        int stage = 0;
+        uint32_t phase = 0;
+        int lt = 0;
+        int fo = 0;  // ordinal of forwarded stage uses (same sequence in all roles)
+        for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+          const int a = lt & 1;
+          const uint32_t use = static_cast<uint32_t>(lt >> 1);
+          mbar_wait(p, tempty + a, (use & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem_base + a * BN;
+          int fwd_nt = -1;
+          if (fwd) {
+            const Tile t = get_tile(p, lin, 0);
+            const int it = t.step % p.T;
+            const int key = kGatherB ? t.pair : t.nt;
+            if (it < p.T - 1 && key < nfwd) fwd_nt = key;
+          }
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            mbar_wait(p, full + stage, phase);
+            tc_fence_after();
+            if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
+              uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kStages + stage;
+              mbar_arrive(fr);
+              mbar_arrive_cluster(mapa_shared(smem_u32(fr), 1));
+              ++fo;
+            }
+            const uint32_t abase = smem_u32(smem_a + stage * kAStageBytes);
+            const uint32_t bbase = smem_u32(smem_b + stage * kBStageBytes);
+  #pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              // A: K-major SW128, 16 elems = 32 B step inside the atom; SBO = 8 rows x 128 B.
+              // MN-major A: like B, 16 K-rows = 2048 B, LBO = 64-row atom (8 KiB), SBO = 1 KiB.
+              const uint64_t ad = kAMn ? make_sdesc(abase + k * 2048, 64 * BK * 2, 1024)
+                                         : make_sdesc(abase + k * 32, 0, 1024);
+              // B: MN-major SW128 (this CTA's 128 columns; the peer holds the other 128 at the
+              // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
+              const uint64_t bd = kBKMajor ? make_sdesc(bbase + k * 32, 0, 1024)
+                                                             : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
+              mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            }
+            mma_commit_2sm(empty + stage, 0x3);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
+          }
+          mma_commit_2sm(tfull + a, 0x3);
+        }
+      }
+    } else {
+      // ===================================================== AG ring forwarders (warps 2-3)
+      // Forwarded stage uses (tile nt < nfwd, k-block kb % nfwd == nt) are split into batches
+      // of fbatch alternating between the two warps. For each of its uses a warp waits on its
+      // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B A image out of SMEM
+      // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4 into
+      // the successor's slot (NVLink peer stores). At the end of its batch (and of every tile)
+      // the warp fences its stores at system scope and publishes the image flags; while one
+      // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
+      // which keeps the ring's progress argument (step-i images depend only on step i-1).
+      if (fwd) {
+        const int grp = warp - 2;
+        uint32_t* unpub[16];
+        int nunpub = 0;
+        uint32_t ph = 0;  // per-stage phase bits of this group's fwd_ready barriers
+        int fo = 0;
+        auto flush = [&]() {
+          const uint64_t tf0 = p.trace ? globaltimer() : 0;
+          fence_sys();
+          __syncwarp();
+          if (lane == 0 && rank != p.fault_rank)
+            for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], ep);
+          if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
+          nunpub = 0;
+        };
+        int lt = 0;
+        for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+          const Tile t = get_tile(p, lin, cta);
+          const int pass = t.step / p.T, it = t.step - pass * p.T;
+          const int key = kGatherB ? t.pair : t.nt;
+          if (!(it < p.T - 1 && key < nfwd)) continue;
+          const int slot = pass * (p.T - 1) + it;
+          const int dst_rank = p.sched[rank][it][0];
+          const uint64_t t0 = p.trace ? globaltimer() : 0;
+          // forwarded operand: this CTA's A rows, or (gather_b) its half of the B tile
+          const bool live = kGatherB ? true : t.valid > 0;
+          const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
+                                          : static_cast<int64_t>(t.mb) * p.nkb;
+          const uint8_t* sbase = kGatherB ? smem_b : smem_a;
+          for (int kb = key; kb < p.nkb; kb += nfwd) {
+            const bool mine = ((fo / fbatch) & 1) == grp;
+            const bool batch_end = (fo % fbatch) == fbatch - 1;
+            ++fo;
+            if (!mine) continue;
+            const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kStages);
+            mbar_wait(p, fwd_ready + grp * kStages + stage, (ph >> stage) & 1u);
+            ph ^= 1u << stage;
+            if (live) {
+              const int64_t img = img0 + kb;
+              const uint4* src = reinterpret_cast<const uint4*>(sbase + stage * kAStageBytes);
+              uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes);
+  #pragma unroll
+              for (int half = 0; half < 2; ++half) {
+                uint4 v[16];
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = src[(half * 16 + i) * 32 + lane];
+  #pragma unroll
+                for (int i = 0; i < 16; ++i) dst[(half * 16 + i) * 32 + lane] = v[i];
+              }
+              unpub[nunpub++] = flag_ptr(p, par, dst_rank, slot, img);
+            }
+            __syncwarp();  // every lane's SMEM reads of the stage are done
+            if (lane == 0) mbar_arrive(empty + stage);
+            if (batch_end && nunpub > 0) flush();
+          }
+          if (nunpub > 0) flush();
+          if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
+        }
       }
     }
   } else {
-    // ===================================================== epilogue (warps 4..7)
-    const int ew = warp - 4;
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsEpi));
+    // ===================================================== epilogue (warps 4..11)
+    // Two warpgroups, one per TMEM accumulator: group eg drains accumulator eg, i.e. this
+    // pair's tiles lt = eg, eg + 2, ... Each group has two main loops' time for one tile's
+    // epilogue (TMEM read, inbox add, wire / output stores, fence + flags), which at short
+    // per-rank K (GEMM-RS at TP = 8) is longer than one main loop.
+    const int eg = (warp - 4) >> 2;
+    const int ew = (warp - 4) & 3;   // TMEM lane quarter this warp may access (warp % 4)
     const int row = ew * 32 + lane;  // row inside this CTA's 128-row block == TMEM lane
     char* out_h = p.out + h * p.out_rank_stride;
     const int64_t esz = p.out_f32 ? 4 : 2;
@@ -700,24 +705,28 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(tempty + 1), 0);
     // RS flags are published lazily: one system fence covers the wire stores of up to
-    // kPend tiles, and pending flags are always published before any wait that may depend
-    // on a peer (so the ring can never wait on itself).
+    // kPend tiles, and pending flags are always published before any wait that may block
+    // (an inbox flag, or an accumulator the other group's progress gates), so the ring can
+    // never wait on itself.
     constexpr int kPend = 2;
     uint32_t* pend[kPend];
     int npend = 0;
     auto publish = [&]() {
       if (npend == 0) return;
+      const uint64_t tp0 = (p.trace && lane == 0) ? globaltimer() : 0;
       fence_sys();
       __syncwarp();
       if (lane == 0 && rank != p.fault_rank)
         for (int i = 0; i < npend; ++i) st_relaxed_sys(pend[i], ep);
+      if (p.trace && lane == 0 && ew == 0) trace_rec(p, TR_PUBLISH, rank, 0, npend, tp0, globaltimer());
       npend = 0;
     };
-    int lt = 0;
-    for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
+    const int a = eg;
+    int lt = eg;
+    for (int lin = gp + eg * GP; lin < ntiles; lin += 2 * GP, lt += 2) {
       const Tile t = get_tile(p, lin, cta);
-      const int a = lt & 1;
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
+      if (npend > 0 && !mbar_try_wait(tfull + a, use & 1)) publish();
       mbar_wait(p, tfull + a, use & 1);
       tc_fence_after();
       const uint64_t t_epi0 = (p.trace && lane == 0) ? globaltimer() : 0;
@@ -821,6 +830,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         else
           rs_epilogue_pipelined<false>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
       }
+      if (p.trace && lane == 0 && ew == 0 && tile_live)
+        trace_rec(p, TR_EPI_LOOP, rank, t.step, lin, t_epi0, globaltimer());
       if (!last && tile_live) {
         pend[npend++] = flag_ptr(p, par, send_rank, slot_send, fidx);
         if (npend == kPend) publish();
@@ -873,11 +884,24 @@ int pdl_setting() {
 bool pdl_enabled() { return pdl_setting() != 0; }
 
 template <int kOp, int kMode>
-void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
+cudaError_t launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   static uint64_t attr_done = 0;
+  static bool pool_ok[64];
   once_per_device(attr_done, [] {
     cudaFuncSetAttribute(tpf_fused_kernel<kOp, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    // the setmaxnreg split must fit the register pool the launch allocates, or
+    // setmaxnreg.inc blocks forever
+    cudaFuncAttributes fa;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    pool_ok[dev & 63] = cudaFuncGetAttributes(&fa, tpf_fused_kernel<kOp, kMode>) == cudaSuccess &&
+                        fa.numRegs * kThreads >= 128 * kRegsCtl + 256 * kRegsEpi;
   });
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!pool_ok[dev & 63]) return cudaErrorInvalidConfiguration;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -896,25 +920,24 @@ void launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   cfg.numAttrs = (pdl_instance(kMode) && pdl_enabled()) ? 2 : 1;
   KParams q = p;
   q.pdl_trigger = pdl_setting() == 3 ? 0 : pdl_setting();
-  cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, q);
+  return cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, q);
 }
 
 }  // namespace
 
-void launch_fused(const KParams& p, int grid, cudaStream_t stream) {
+cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream) {
   switch (p.mode) {
-    case MODE_DP_GRAD: launch_instance<OP_RS, MODE_DP_GRAD>(p, grid, stream); return;
-    case MODE_GATHER_B: launch_instance<OP_AG, MODE_GATHER_B>(p, grid, stream); return;
-    case MODE_QK: launch_instance<OP_RS, MODE_QK>(p, grid, stream); return;
-    case MODE_PV: launch_instance<OP_RS, MODE_PV>(p, grid, stream); return;
-    case MODE_QSPLIT: launch_instance<OP_RS, MODE_QSPLIT>(p, grid, stream); return;
+    case MODE_DP_GRAD: return launch_instance<OP_RS, MODE_DP_GRAD>(p, grid, stream);
+    case MODE_GATHER_B: return launch_instance<OP_AG, MODE_GATHER_B>(p, grid, stream);
+    case MODE_QK: return launch_instance<OP_RS, MODE_QK>(p, grid, stream);
+    case MODE_PV: return launch_instance<OP_RS, MODE_PV>(p, grid, stream);
+    case MODE_QSPLIT: return launch_instance<OP_RS, MODE_QSPLIT>(p, grid, stream);
     case MODE_SINGLE:
-      if (p.op == OP_AG) launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream);
-      else launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);
-      return;
+      return p.op == OP_AG ? launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream)
+                           : launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);
     default:
-      if (p.op == OP_AG) launch_instance<OP_AG, MODE_STD>(p, grid, stream);
-      else launch_instance<OP_RS, MODE_STD>(p, grid, stream);
+      return p.op == OP_AG ? launch_instance<OP_AG, MODE_STD>(p, grid, stream)
+                           : launch_instance<OP_RS, MODE_STD>(p, grid, stream);
   }
 }
 

@@ -197,15 +197,6 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Pins registers written by an in-flight tcgen05.ld behind the tcgen05.wait::ld that
-// completes it. The compiler treats the ld's outputs as available at once, so when the
-// next chunk's ld is issued before the current chunk is processed (software pipelining)
-// it could otherwise schedule arithmetic on them ahead of the wait.
-__device__ __forceinline__ void tmem_regs_pin(uint32_t (&r)[32]) {
-#pragma unroll
-  for (int i = 0; i < 32; ++i) asm volatile("" : "+r"(r[i]));
-}
-
 // UMMA shared-memory matrix descriptor (sm_100: version bits [46,48) = 1).
 // layout: 2 = SWIZZLE_128B. Addresses / offsets in bytes.
 __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {

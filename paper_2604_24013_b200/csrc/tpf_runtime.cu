@@ -400,8 +400,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
                                 std::to_string(R) + " resident CTA pairs, device has " +
                                 std::to_string(pairs));
   p.ctas_per_rank = 2 * pairs_per_rank;
-  tpf::launch_fused(p, p.ctas_per_rank * R, stream);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = tpf::launch_fused(p, p.ctas_per_rank * R, stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return tpf::Status::cuda(std::string("kernel launch: ") + cudaGetErrorString(e));
   return tpf::Status::ok();
 }

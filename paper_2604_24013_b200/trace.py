@@ -14,8 +14,10 @@ from collections import defaultdict
 from dataclasses import dataclass
 
 TR_TILE, TR_MAINLOOP, TR_AG_PIECE, TR_WAIT_A, TR_WAIT_IN, TR_FLAG = 1, 2, 3, 4, 5, 6
+TR_FLUSH, TR_EPI_LOOP, TR_PUBLISH = 7, 8, 9
 KIND_NAMES = {TR_TILE: "tile", TR_MAINLOOP: "mainloop", TR_AG_PIECE: "ag_piece",
-              TR_WAIT_A: "wait_wire", TR_WAIT_IN: "wait_inbox", TR_FLAG: "flag"}
+              TR_WAIT_A: "wait_wire", TR_WAIT_IN: "wait_inbox", TR_FLAG: "flag",
+              TR_FLUSH: "ag_flush", TR_EPI_LOOP: "rs_epilogue_loop", TR_PUBLISH: "rs_publish"}
 
 
 @dataclass

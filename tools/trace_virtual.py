@@ -60,6 +60,11 @@ def show(name, fn, compute_only=False):
           f"MMA gap between tiles mean {sum(gaps) / max(1, len(gaps)):.2f} max {max(gaps or [0]):.2f} us, "
           f"first main loop starts {min(first):.1f}-{max(first):.1f} us, last ends {min(last):.1f}-{max(last):.1f} us",
           flush=True)
+    for kind in (trace.TR_EPI_LOOP, trace.TR_PUBLISH, trace.TR_FLUSH, trace.TR_WAIT_IN, trace.TR_WAIT_A):
+        rr = [r for r in recs if r.kind == kind]
+        if rr:
+            print(f"    {trace.KIND_NAMES[kind]}: {len(rr)} records, mean {sum(r.t1 - r.t0 for r in rr) / len(rr) / 1e3:.2f} us, "
+                  f"max {max(r.t1 - r.t0 for r in rr) / 1e3:.2f} us", flush=True)
 
 
 show("AG", lambda: comm.ag_gemm(x, w, y))
