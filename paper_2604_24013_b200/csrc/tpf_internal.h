@@ -14,8 +14,8 @@ constexpr int BK = 64;           // 64 bf16 = one 128 B swizzle atom row
 constexpr int kStages = 6;
 constexpr int kThreads = 384;    // 12 warps: TMA, MMA, 2x comm, 2 x 4 epilogue (one group per accumulator)
 constexpr int kRegPool = 168;    // registers per thread the launch allocates (__launch_bounds__(384, 1))
-constexpr int kRegsCtl = 80;     // setmaxnreg: warps 0-3 (the AG forwarders spill below 80)
-constexpr int kRegsEpi = 208;    // setmaxnreg: epilogue warpgroups (128 * 80 + 256 * 208 <= 384 * 168)
+constexpr int kRegsCtl = 88;     // setmaxnreg: warps 0-3 (the AG producer / forwarders spill below 88)
+constexpr int kRegsEpi = 208;    // setmaxnreg: epilogue warpgroups (128 * 88 + 256 * 208 == 384 * 168)
 static_assert(128 * kRegsCtl + 256 * kRegsEpi <= kThreads * kRegPool, "setmaxnreg split exceeds the pool");
 constexpr int kAStageBytes = BM * BK * 2;        // 16 KiB: also the AG wire "image" unit
 constexpr int kBStageBytes = (BN / 2) * BK * 2;  // 16 KiB: this CTA's half of B
