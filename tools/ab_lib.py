@@ -1,7 +1,8 @@
 """Dev tool: A/B two library builds on the per-GPU TP = 8 fused ops (virtual peers, cfg2 and
 cfg3 shapes, AG-GEMM and GEMM-RS), alternating processes to cancel power-cap drift. Prints
 the median us per call (20 back-to-back calls) for each build.
-    python tools/ab_lib.py LIB_A LIB_B [rounds]"""
+    python tools/ab_lib.py LIB_A LIB_B [rounds]
+A spec may carry environment settings: 'lib.so@TPF_AG_SPLIT=0@TPF_X=1'."""
 import json
 import os
 import statistics
@@ -46,7 +47,9 @@ rounds = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 res = {lib: [] for lib in libs}
 for _ in range(rounds):
     for lib in libs:
-        env = dict(os.environ, TPF_LIB_PATH=os.path.abspath(lib))
+        path, *kvs = lib.split("@")
+        env = dict(os.environ, TPF_LIB_PATH=os.path.abspath(path))
+        env.update(kv.split("=", 1) for kv in kvs)
         out = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True, timeout=600)
         try:
             res[lib].append(json.loads(out.stdout.strip().splitlines()[-1]))
