@@ -1,6 +1,6 @@
 """Dev tool: one fused AG-GEMM and one fused GEMM-RS of a TP group's rank 0 with virtual peers
 (cfg2 shapes), for an ncu capture of the protocol at full-GPU scale.
-    python tools/ncu_virtual_ops.py T"""
+    python tools/ncu_virtual_ops.py T [co]   (co: also one compute-only AG-GEMM, for a side-by-side)"""
 import os
 import sys
 
@@ -23,6 +23,10 @@ comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, D, 2 * F 
                                              tpf.sym_bytes_rs(T, 1, S, F // T, D, 1, tpf.BF16)))
 comm.ag_gemm(x, w, y)
 comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16)
+if len(sys.argv) > 2 and sys.argv[2] == "co":
+    comm.set_compute_only(True)
+    comm.ag_gemm(x, w, y)
+    comm.set_compute_only(False)
 torch.cuda.synchronize()
 comm.close()
 print("ok")

@@ -60,6 +60,12 @@ def show(name, fn, compute_only=False):
           f"MMA gap between tiles mean {sum(gaps) / max(1, len(gaps)):.2f} max {max(gaps or [0]):.2f} us, "
           f"first main loop starts {min(first):.1f}-{max(first):.1f} us, last ends {min(last):.1f}-{max(last):.1f} us",
           flush=True)
+    # per-pair load balance: total producer main-loop time per block, and the blocks
+    # (SM placement follows blockIdx) that finish last
+    busy = sorted((sum(r.t1 - r.t0 for r in v) / 1e3, b) for b, v in by.items())
+    fin = sorted(((max(r.t1 for r in v) - t0) / 1e3, b) for b, v in by.items())
+    print(f"    per-block main-loop busy: min {busy[0][0]:.1f} median {busy[len(busy) // 2][0]:.1f} max {busy[-1][0]:.1f} us;"
+          f" slowest blocks {[b for _, b in busy[-6:]]}, last to finish {[b for _, b in fin[-6:]]}", flush=True)
     for kind in (trace.TR_EPI_LOOP, trace.TR_PUBLISH, trace.TR_FLUSH, trace.TR_WAIT_IN, trace.TR_WAIT_A):
         rr = [r for r in recs if r.kind == kind]
         if rr:
