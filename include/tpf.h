@@ -121,11 +121,6 @@ int tpf_comm_set_compute_only(tpf_comm* c, int on);
  * wait on an AG wire image, 5 epilogue wait on an RS inbox, 6 RS flag published.
  * NULL disables (default). Used for the measured no-tail check. */
 int tpf_comm_set_trace(tpf_comm* c, void* buffer, int64_t capacity_records);
-/* Diagnostic: K-split parts per tail tile of the last fused AG-GEMM launched on this
- * communicator (0: no split tail). When the last round of pair tiles fills at most half
- * the CTA pairs, each of its tiles is computed as S K-slices on S pairs and reduced in a
- * fixed order (TPF_AG_SPLIT=0 disables). */
-int tpf_comm_last_split(const tpf_comm* c);
 
 /* -------------------------------------------------------------- fused ops
  * AG-GEMM. Replaces:

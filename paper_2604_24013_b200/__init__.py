@@ -72,7 +72,6 @@ _lib.tpf_comm_set_timeout_ns.argtypes = [_vp, _i64]
 _lib.tpf_comm_inject_fault.argtypes = [_vp, C.c_int]
 _lib.tpf_comm_set_compute_only.argtypes = [_vp, C.c_int]
 _lib.tpf_comm_set_trace.argtypes = [_vp, _vp, _i64]
-_lib.tpf_comm_last_split.argtypes = [_vp]
 _lib.tpf_ag_gemm.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 3 + [_vp]
 _lib.tpf_gemm_rs.argtypes = [_vp, _vp, _vp, _vp] + [_i64] * 4 + [C.c_int] * 4 + [_vp]
 _lib.tpf_gemm.argtypes = [_vp, _vp, _vp] + [_i64] * 3 + [C.c_int, _vp]
@@ -112,7 +111,6 @@ EXPORTED_SYMBOLS = (
     "tpf_comm_inject_fault",
     "tpf_comm_set_compute_only",
     "tpf_comm_set_trace",
-    "tpf_comm_last_split",
     "tpf_ag_gemm",
     "tpf_gemm_rs",
     "tpf_dp_grad_rs",
@@ -247,10 +245,6 @@ class Communicator:
     def set_compute_only(self, on: bool) -> None:
         """Measurement hook: same kernels, no flag waits / wire traffic (exposed-comm baseline)."""
         _check(_lib.tpf_comm_set_compute_only(self._h, int(bool(on))))
-
-    def last_split_parts(self) -> int:
-        """K-split parts per tail tile of the last fused AG-GEMM on this communicator (0: none)."""
-        return int(_lib.tpf_comm_last_split(self._h))
 
     def set_trace(self, buf) -> None:
         """Attach a zeroed device int64 tensor of (cap+1)*4 words as the timeline trace (None: off)."""

@@ -41,12 +41,6 @@ enum Mode : int {
 //   [1] rank  [2] step  [3] tile / piece  [4] abort flag
 constexpr int kErrWords = 8;
 
-// Split-tail workspace per hosted rank: at most one partial per CTA pair, i.e. kMaxPairs
-// pair tiles of 2 x 128 x 256 fp32, and 2 x 2 x 4 counters per tail tile.
-constexpr int kMaxPairs = 128;
-constexpr int64_t kSplitWsFloatsPerRank = static_cast<int64_t>(kMaxPairs) * 2 * 128 * 256;
-constexpr int kSplitCntPerRank = kMaxPairs * 16;
-
 struct KParams {
   CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); a_mn: (rows, K, B, ranks)
   CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); b_kmajor: (K, N, ranks)
@@ -108,14 +102,6 @@ struct KParams {
   int fault_rank;   // test hook: this rank never publishes its flags (-1: none)
   int compute_only; // measurement: same tiles, no flag waits / wire traffic (exposed-comm baseline)
   int pdl_trigger;  // PDL instances: 1 trigger the next launch after the prologue, 2 after the last TMA load, 0 at exit
-  // AG split tail: the last round's tiles (all in the final step, which forwards nothing)
-  // are split along K into split_s parts on split_s pairs each; every part stores its fp32
-  // partial, then each part reduces some of the tile's column chunks in a fixed order.
-  int split_s;         // parts per tail tile (0: off)
-  int split_base;      // first tail tile (tiles [split_base, ntiles) are split)
-  float* split_ws;     // per hosted rank: split_ws_stride floats of partial-tile images
-  int64_t split_ws_stride;
-  uint32_t* split_cnt; // per hosted rank: kSplitCntPerRank counters (arrivals, done)
   // Optional device trace (%globaltimer ns): records of 4 x u64 appended via trace[0] counter.
   unsigned long long* trace;
   int64_t trace_cap;  // records

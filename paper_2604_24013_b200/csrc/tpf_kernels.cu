@@ -77,26 +77,6 @@ __device__ __forceinline__ Tile get_tile(const KParams& p, int lin, int cta) {
   return t;
 }
 
-// Work item of a CTA pair: a whole tile, or (split tail) part q of a tail tile with
-// k-blocks [kb0, kb1).
-struct Item {
-  int lin, kb0, kb1, part;  // part: -1 whole tile
-};
-
-__device__ __forceinline__ int items_of_pair(const KParams& p, int gp, int GP, int ntiles) {
-  const int limit = p.split_s ? p.split_base : ntiles;
-  int n = limit > gp ? (limit - gp + GP - 1) / GP : 0;
-  if (p.split_s && gp < (ntiles - limit) * p.split_s) ++n;
-  return n;
-}
-
-__device__ __forceinline__ Item item_of_pair(const KParams& p, int gp, int GP, int i) {
-  const int lin = gp + i * GP;
-  if (!p.split_s || lin < p.split_base) return Item{lin, 0, p.nkb, -1};
-  const int S = p.split_s, q = gp % S;
-  return Item{p.split_base + gp / S, q * p.nkb / S, (q + 1) * p.nkb / S, q};
-}
-
 __device__ __forceinline__ void trace_rec(const KParams& p, int kind, int rank, int step,
                                           int64_t index, uint64_t t0, uint64_t t1) {
   if (!p.trace) return;
@@ -270,94 +250,6 @@ __device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0,
 }
 
 }  // namespace
-
-// AG split tail, one part (q of split_s) of tail tile u, this warp's 32 rows: store the fp32
-// partial (TMEM fragment image: [32-col chunk j][16-B group g][row][16 B], coalesced), release
-// the accumulator, count the part in, wait for all parts, then reduce the column chunks
-// j = q, q + S, ... over the parts in a fixed order (part 0 first) and run the AG epilogue
-// on them. The last part through resets the counters for the next call (kernel-ordered).
-// Not inlined: keeps its registers out of the hot epilogue.
-__device__ __noinline__ void ag_split_epilogue(const KParams& p, uint32_t taddr, int h, int rank, int u, int q,
-                                               int cta, int ew, int row, bool valid, char* rp, int64_t col0,
-                                               uint32_t tempty_a, int step, int lin) {
-  const int S = p.split_s;
-  const int lane = threadIdx.x & 31;
-  constexpr int64_t kHalf = static_cast<int64_t>(BM) * BN;  // floats of one CTA's partial
-  float* ws = p.split_ws + h * p.split_ws_stride;
-  float* mine = ws + (static_cast<int64_t>(u) * S + q) * 2 * kHalf + cta * kHalf;
-  for (int j = 0; j < BN / 32; ++j) {
-    uint32_t r[32];
-    tmem_ld_32x32b_x32(taddr + j * 32, r);
-    tmem_ld_wait();
-#pragma unroll
-    for (int g = 0; g < 8; ++g)
-      *reinterpret_cast<float4*>(mine + ((j * 8 + g) * BM + row) * 4) =
-          make_float4(__uint_as_float(r[4 * g]), __uint_as_float(r[4 * g + 1]), __uint_as_float(r[4 * g + 2]),
-                      __uint_as_float(r[4 * g + 3]));
-  }
-  tc_fence_before();
-  __syncwarp();
-  if (lane == 0) mbar_arrive_cluster(tempty_a);
-  uint32_t* cnt = p.split_cnt + h * kSplitCntPerRank + (u * 2 + cta) * 8 + ew;  // arrivals
-  uint32_t* done = cnt + 4;                                                    // reducers finished
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) {
-    atomicAdd(cnt, 1u);
-    const uint64_t t0 = globaltimer();
-    while (ld_acquire_gpu(cnt) < static_cast<uint32_t>(S)) {
-      if (aborted(p)) break;
-      if (globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns)) {
-        record_error(p, 2, rank, step, lin);
-        break;
-      }
-      __nanosleep(64);
-    }
-  }
-  __syncwarp();
-  (void)ld_acquire_gpu(cnt);  // every lane reads the partials after observing all arrivals
-  const bool swiglu = p.act == ACT_SWIGLU;
-  const int nchunks = swiglu ? BN / 64 : BN / 32;
-  for (int j = q; j < nchunks; j += S) {
-    float acc[32], up[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) { acc[c] = 0.f; up[c] = 0.f; }
-#pragma unroll 2
-    for (int qq = 0; qq < S; ++qq) {
-      const float* part = ws + static_cast<int64_t>(u * S + qq) * 2 * kHalf + cta * kHalf;
-      float4 v[8], w[8];
-#pragma unroll
-      for (int g = 0; g < 8; ++g) v[g] = *reinterpret_cast<const float4*>(part + ((j * 8 + g) * BM + row) * 4);
-      if (swiglu) {
-#pragma unroll
-        for (int g = 0; g < 8; ++g)
-          w[g] = *reinterpret_cast<const float4*>(part + (((j + BN / 64) * 8 + g) * BM + row) * 4);
-      }
-#pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        acc[4 * g] += v[g].x; acc[4 * g + 1] += v[g].y; acc[4 * g + 2] += v[g].z; acc[4 * g + 3] += v[g].w;
-      }
-      if (swiglu) {
-#pragma unroll
-        for (int g = 0; g < 8; ++g) {
-          up[4 * g] += w[g].x; up[4 * g + 1] += w[g].y; up[4 * g + 2] += w[g].z; up[4 * g + 3] += w[g].w;
-        }
-      }
-    }
-    float o[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      const float x = acc[c];
-      o[c] = swiglu ? __fdividef(x, 1.0f + __expf(-x)) * up[c] : (p.act == ACT_SQUARE ? x * x : x);
-    }
-    if (valid) store_out_row(p, rp, col0 + j * 32, o);
-  }
-  __syncwarp();
-  if (lane == 0 && atomicAdd(done, 1u) == static_cast<uint32_t>(S - 1)) {
-    *cnt = 0u;
-    *done = 0u;
-  }
-}
 
 // rs_direct last step: fold the T-1 received partials into the own one, sub-chunk by
 // sub-chunk. Not inlined: its T-1 in-flight inbox loads per sub-chunk would otherwise add
@@ -559,10 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
       int stage = 0;
       uint32_t phase = 0;
-      const int nitems = items_of_pair(p, gp, GP, ntiles);
-      for (int ii = 0; ii < nitems && (warp_walk || lane == 0); ++ii) {
-        const Item w = item_of_pair(p, gp, GP, ii);
-        const int lin = w.lin;
+      for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
         const bool from_wire = !kSingle && (kOp == OP_AG) && it > 0 && !p.compute_only;
@@ -584,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                                         : static_cast<int64_t>(t.mb) * p.nkb;
         const bool wire_live = a_from_wire ? (t.valid > 0) : b_from_wire;
         const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
-        int ready = w.kb0 - 1;  // wire images [kb0, ready] of this operand block are known to have landed
+        int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
         uint64_t t_first = 0;
         const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
         const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
@@ -606,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           }
           fence_proxy_async_global();
         }
-        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+        for (int kb = 0; kb < p.nkb; ++kb) {
           if (wire_live && kb > ready) {
             // Claim the run of consecutive landed images from kb on: every lane acquire-loads
             // one flag (image kb + lane, system scope; one round trip per poll) until image
@@ -684,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                                   kb * BK, h);
               }
             }
-            if (p.trace && kb == w.kb0) t_first = globaltimer();
+            if (p.trace && kb == 0) t_first = globaltimer();
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -700,10 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         uint32_t phase = 0;
         int lt = 0;
         int fo = 0;  // ordinal of forwarded stage uses (same sequence in all roles)
-        const int nitems = items_of_pair(p, gp, GP, ntiles);
-        for (int ii = 0; ii < nitems; ++ii, ++lt) {
-          const Item w = item_of_pair(p, gp, GP, ii);
-          const int lin = w.lin;
+        for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
           const int a = lt & 1;
           const uint32_t use = static_cast<uint32_t>(lt >> 1);
           mbar_wait(p, tempty + a, (use & 1) ^ 1);
@@ -716,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
             const int key = kGatherB ? t.pair : t.nt;
             if (it < p.T - 1 && key < nfwd) fwd_nt = key;
           }
-          for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(p, full + stage, phase);
             tc_fence_after();
             if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
@@ -737,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
               // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
               const uint64_t bd = kBKMajor ? make_sdesc(bbase + k * 32, 0, 1024)
                                                              : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
-              mma_bf16_2sm(d, ad, bd, idesc, (kb != w.kb0 || k != 0) ? 1u : 0u);
+              mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
             mma_commit_2sm(empty + stage, 0x3);
             if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -770,11 +656,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
           nunpub = 0;
         };
-        // split-tail items (the final step) forward nothing, and every item before them is
-        // a whole tile of nkb stages, so the stage ordinal below stays (lt * nkb + kb)
-        const int limit = p.split_s ? p.split_base : ntiles;
         int lt = 0;
-        for (int lin = gp; lin < limit; lin += GP, ++lt) {
+        for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
           const Tile t = get_tile(p, lin, cta);
           const int pass = t.step / p.T, it = t.step - pass * p.T;
           const int key = kGatherB ? t.pair : t.nt;
@@ -851,10 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       npend = 0;
     };
     const int a = eg;
-    const int nitems = items_of_pair(p, gp, GP, ntiles);
-    for (int lt = eg; lt < nitems; lt += 2) {
-      const Item w = item_of_pair(p, gp, GP, lt);
-      const int lin = w.lin;
+    int lt = eg;
+    for (int lin = gp + eg * GP; lin < ntiles; lin += 2 * GP, lt += 2) {
       const Tile t = get_tile(p, lin, cta);
       const uint32_t use = static_cast<uint32_t>(lt >> 1);
       if (npend > 0 && !mbar_try_wait(tfull + a, use & 1)) publish();
@@ -875,14 +756,6 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                                         : static_cast<int64_t>(t.b) * p.out_rows +
                                               (static_cast<int64_t>(l) * p.m + pass) * p.Sc + t.row0 + row;
         char* rp = out_h + (orow * p.out_ld + (kGatherB ? static_cast<int64_t>(l) * p.blk_cols : 0)) * esz;
-        if (w.part >= 0) {
-          const int64_t col0 = static_cast<int64_t>(t.nt) * (p.act == ACT_SWIGLU ? BN / 2 : BN);
-          ag_split_epilogue(p, taddr, h, rank, lin - p.split_base, w.part, cta, ew, row, valid, rp, col0,
-                            a ? tempty_leader1 : tempty_leader0, t.step, lin);
-          if (p.trace && lane == 0 && ew == 0 && tile_live)
-            trace_rec(p, TR_TILE, rank, t.step, lin, t_epi0, globaltimer());
-          continue;
-        }
         if (p.act == ACT_SWIGLU) {
           // Tile-interleaved W: columns [0,128) of the tile are gate, [128,256) the matching
           // up columns -> 128 output columns silu(gate) * up (Llama MLP, fused).

@@ -154,35 +154,9 @@ struct tpf_comm {
   size_t scratch_bytes = 0;
   unsigned long long* trace = nullptr;
   int64_t trace_cap = 0;
-  float* split_ws = nullptr;      // AG split-tail partials, split_ws_stride floats per hosted rank
-  int64_t split_ws_stride = 0;
-  uint32_t* split_cnt = nullptr;  // AG split-tail counters, kSplitCntPerRank per hosted rank
-  int last_split = 0;             // split parts of the last AG launch (diagnostic)
 };
 
 namespace {
-
-// AG split-tail workspace: one fp32 pair-tile partial per resident CTA pair of each hosted
-// rank, plus zeroed counters.
-cudaError_t alloc_split(tpf_comm* c, int hosted) {
-  const int pairs = std::max(1, tpf::max_pairs() / hosted);
-  c->split_ws_stride = static_cast<int64_t>(std::min(pairs, tpf::kMaxPairs)) * 2 * tpf::BM * tpf::BN;
-  cudaError_t e = cudaMalloc(&c->split_ws, static_cast<size_t>(c->split_ws_stride) * hosted * sizeof(float));
-  if (e == cudaSuccess)
-    e = cudaMalloc(&c->split_cnt, static_cast<size_t>(tpf::kSplitCntPerRank) * hosted * sizeof(uint32_t));
-  if (e == cudaSuccess)
-    e = cudaMemset(c->split_cnt, 0, static_cast<size_t>(tpf::kSplitCntPerRank) * hosted * sizeof(uint32_t));
-  return e;
-}
-
-// TPF_AG_SPLIT=0 turns the AG split tail off (A/B switch).
-bool split_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("TPF_AG_SPLIT");
-    return !(e && e[0] == '0');
-  }();
-  return on;
-}
 
 struct Geometry {
   int nmb_per_batch, nmb, nnt, nkb, npairs;
@@ -350,11 +324,6 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.compute_only = c ? c->compute_only : 0;
   p.trace = c ? c->trace : nullptr;
   p.trace_cap = c ? c->trace_cap : 0;
-  p.split_s = 0;
-  p.split_base = 0;
-  p.split_ws = c ? c->split_ws : nullptr;
-  p.split_ws_stride = c ? c->split_ws_stride : 0;
-  p.split_cnt = c ? c->split_cnt : nullptr;
   if (k.T > 1) {
     for (int r = 0; r < k.T; ++r)
       for (int i = 0; i < k.T; ++i)
@@ -431,24 +400,6 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
                                 std::to_string(R) + " resident CTA pairs, device has " +
                                 std::to_string(pairs));
   p.ctas_per_rank = 2 * pairs_per_rank;
-  if (p.mode == tpf::MODE_STD && p.op == tpf::OP_AG && p.split_ws && split_enabled()) {
-    // Split tail: when the last round of pair tiles fills at most half the pairs, split each
-    // of its tiles along K over S = pairs / tail pairs (>= 2 k-blocks per part). The tail
-    // must lie in the final step, which forwards nothing.
-    const int GP = pairs_per_rank;
-    const int per_step = p.npairs * p.nnt;
-    const int ntiles = p.nsteps * per_step;
-    const int rounds = (ntiles + GP - 1) / GP;
-    const int tail = ntiles - (rounds - 1) * GP;
-    const int S = std::min(GP / tail, p.nkb / 2);
-    if (rounds >= 2 && tail <= per_step && S >= 2 &&
-        static_cast<int64_t>(tail) * S * 2 * tpf::BM * tpf::BN <= p.split_ws_stride &&
-        tail * 2 * 8 <= tpf::kSplitCntPerRank) {
-      p.split_s = S;
-      p.split_base = ntiles - tail;
-    }
-  }
-  if (c && p.op == tpf::OP_AG) c->last_split = p.split_s;
   cudaError_t e = tpf::launch_fused(p, p.ctas_per_rank * R, stream);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return tpf::Status::cuda(std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -529,14 +480,11 @@ int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = alloc_split(c, 1);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
     if (c->err) cudaFree(c->err);
     if (c->dev_epoch) cudaFree(c->dev_epoch);
-    if (c->split_ws) cudaFree(c->split_ws);
-    if (c->split_cnt) cudaFree(c->split_cnt);
     delete c;
     return fail(tpf::Status::cuda(std::string("tpf_comm_create: ") + cudaGetErrorString(e)));
   }
@@ -594,14 +542,11 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = alloc_split(c, world);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     if (c->local) cudaFree(c->local);
     if (c->err) cudaFree(c->err);
     if (c->dev_epoch) cudaFree(c->dev_epoch);
-    if (c->split_ws) cudaFree(c->split_ws);
-    if (c->split_cnt) cudaFree(c->split_cnt);
     delete c;
     return fail(tpf::Status::cuda(std::string("tpf_comm_create_local_group: ") + cudaGetErrorString(e)));
   }
@@ -647,8 +592,6 @@ int tpf_comm_destroy(tpf_comm* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->scratch) cudaFree(c->scratch);
-  if (c->split_ws) cudaFree(c->split_ws);
-  if (c->split_cnt) cudaFree(c->split_cnt);
   delete c;
   return TPF_OK;
 }
@@ -668,8 +611,6 @@ int tpf_comm_set_trace(tpf_comm* c, void* buffer, int64_t capacity_records) {
   c->trace_cap = buffer ? capacity_records : 0;
   return TPF_OK;
 }
-
-int tpf_comm_last_split(const tpf_comm* c) { return c ? c->last_split : -1; }
 
 int tpf_comm_set_compute_only(tpf_comm* c, int on) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));

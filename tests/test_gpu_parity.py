@@ -372,92 +372,6 @@ def test_full_size_cfg2_ag_gemm_bitexact_vs_gemm():
     assert (out[0, 0].float() - ref32).abs().max().item() <= 2e-2 * ref32.abs().max().item()
 
 
-# ------------------------------------------------ AG split tail (last round split along K)
-# T = 2 local group (37 pairs per rank): Sc = 512 rows (2 pair rows) x N_l = 2560 (10 n-tiles)
-# gives 20 tiles per step, 40 per rank: rounds of 37 leave a tail of 3 tiles, each split over
-# min(37 // 3, nkb // 2) pairs.
-SPLIT_T, SPLIT_S, SPLIT_N = 2, 1024, 5120
-
-
-@pytest.mark.parametrize("K", [512, 1000])
-def test_ag_split_tail_exact(K):
-    """The split tail's fixed-order fp32 reduction of K-slices is exact on integer data."""
-    T, S, N = SPLIT_T, SPLIT_S, SPLIT_N
-    x = O.randint((1, S, K), 0, 5, 31)
-    w = O.randint((K, N), -2, 2, 32)
-    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, 1, S, K, N // T, 1))
-    got = run_ag(T, 1, x, w, comm=comm)
-    parts = comm.last_split_parts()
-    comm.close()
-    assert parts >= 2, parts
-    assert np.array_equal(got, O.column_parallel(T, 1, x, w))
-
-
-def test_ag_split_tail_random_and_swiglu():
-    """Random data: split-tail tiles within fp32 rounding of the unsplit GEMM, and the fused
-    SwiGLU epilogue on split tiles matches torch."""
-    T, S, K, N = SPLIT_T, SPLIT_S, 768, SPLIT_N
-    g = torch.Generator(device=DEV).manual_seed(5)
-    x = torch.randn((T, 1, S // T, K), device=DEV, generator=g).to(torch.bfloat16)
-    w = (torch.randn((T, K, N // T), device=DEV, generator=g) / K ** 0.5).to(torch.bfloat16)
-    out = torch.empty((T, 1, S, N // T), device=DEV, dtype=torch.float32)
-    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, 1, S, K, N // T, 1))
-    comm.ag_gemm(x, w, out)
-    comm.sync()
-    assert comm.last_split_parts() >= 2
-    xg = x.reshape(S, K)
-    for r in range(T):
-        ref = torch.empty((S, N // T), device=DEV, dtype=torch.float32)
-        tpf.gemm(xg, w[r], ref)
-        err = (out[r, 0] - ref).abs().max().item()
-        assert err <= 1e-5 * ref.abs().max().item(), (r, err)
-    gate, up = w[..., : N // (2 * T)], w[..., N // (2 * T):]
-    wi = torch.stack([tpf.interleave_gate_up(gate[r], up[r]) for r in range(T)]).contiguous()
-    act = torch.empty((T, 1, S, N // (2 * T)), device=DEV, dtype=torch.float32)
-    comm.ag_gemm(x, wi, act, act=tpf.ACT_SWIGLU)
-    comm.sync()
-    assert comm.last_split_parts() >= 2
-    comm.close()
-    for r in range(T):
-        gg, uu = xg.float() @ gate[r].float(), xg.float() @ up[r].float()
-        ref = torch.nn.functional.silu(gg) * uu
-        err = (act[r, 0] - ref).abs().max().item()
-        assert err <= 1e-3 * ref.abs().max().item() + 1e-5, (r, err)
-
-
-def test_ag_split_tail_repeated_calls_and_graph():
-    """Counters reset between calls: back-to-back eager calls and CUDA-graph replays of a
-    split-tail AG-GEMM stay exact on integer data."""
-    T, S, K, N = SPLIT_T, SPLIT_S, 512, SPLIT_N
-    x = O.randint((1, S, K), 0, 5, 41)
-    w = O.randint((K, N), -2, 2, 42)
-    want = O.column_parallel(T, 1, x, w)
-    sl, nl = S // T, N // T
-    xs = torch.stack([bf16(x[:, r * sl:(r + 1) * sl]) for r in range(T)]).to(DEV)
-    ws = torch.stack([bf16(w[:, r * nl:(r + 1) * nl]) for r in range(T)]).to(DEV)
-    out = torch.empty((T, 1, S, nl), device=DEV, dtype=torch.float32)
-    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, 1, S, K, nl, 1))
-    for _ in range(5):
-        out.fill_(float("nan"))
-        comm.ag_gemm(xs, ws, out)
-        comm.sync()
-        assert np.array_equal(out.double().cpu().numpy(), want)
-    st = torch.cuda.Stream(device=DEV)
-    with torch.cuda.stream(st):
-        comm.ag_gemm(xs, ws, out, stream=st)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=st):
-        comm.ag_gemm(xs, ws, out, stream=st)
-    for _ in range(3):
-        out.fill_(float("nan"))
-        graph.replay()
-        torch.cuda.synchronize()
-        assert np.array_equal(out.double().cpu().numpy(), want)
-    comm.sync()
-    comm.close()
-
-
 def test_swiglu_matches_torch():
     gu = torch.randn((1000, 2 * 1792), device=DEV).to(torch.bfloat16)
     out = torch.empty((1000, 1792), device=DEV, dtype=torch.bfloat16)

@@ -1,4 +1,4 @@
-"""Dev tool: A/B two library builds on the per-GPU TP = 8 fused ops (virtual peers, cfg2 and
+"""Dev tool: A/B two library builds on the per-GPU TP = 8 (AB_T) fused ops (virtual peers, cfg2 and
 cfg3 shapes, AG-GEMM and GEMM-RS), alternating processes to cancel power-cap drift. Prints
 the median us per call (20 back-to-back calls) for each build.
     python tools/ab_lib.py LIB_A LIB_B [rounds]
@@ -23,7 +23,7 @@ def loop(fn, n=20):
     e1.record(); torch.cuda.synchronize()
     return 1e3 * e0.elapsed_time(e1) / n
 res = {}
-T = 8
+T = int(os.environ.get("AB_T", "8"))
 for cfg, S, K_ag, N_ag, K_rs, N_rs in (("cfg2", 8192, 4096, 28672, 14336, 4096), ("cfg3", 16384, 8192, 10240, 8192, 8192)):
     g = torch.Generator(device=dev).manual_seed(0)
     x = torch.randn((1, S // T, K_ag), device=dev, generator=g).to(torch.bfloat16)
