@@ -39,6 +39,9 @@ for cfg, S, K_ag, N_ag, K_rs, N_rs in (("cfg2", 8192, 4096, 28672, 14336, 4096),
     res[cfg + "_ag"] = loop(lambda: comm.ag_gemm(x, w, y))
     res[cfg + "_rs"] = loop(lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16))
     res[cfg + "_ag_gemm"] = loop(lambda: tpf.gemm(xg, w, yg))
+    comm.set_compute_only(True)
+    res[cfg + "_ag_co"] = loop(lambda: comm.ag_gemm(x, w, y))
+    comm.set_compute_only(False)
     comm.close()
 print(json.dumps(res))
 '''
