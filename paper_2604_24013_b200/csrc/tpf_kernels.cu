@@ -393,7 +393,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   // successor before the stage is recycled (so `empty` also waits for the forwarder).
   const bool fwd = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
   const int nfwd = min(p.ag_nfwd, p.nnt);       // leading n-tiles that forward an m-block
-  const int fbatch = min(max(p.ag_batch, 1), 16);  // forwards per fence + flag publication
+  const int fbatch = min(max(p.ag_batch, 1), 8);  // forwards per fence + flag publication
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&p.tmap_a);
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(full + s, 2);
-      mbar_init(empty + s, fwd ? 2 : 1);
+      mbar_init(empty + s, (fwd && kGatherB) ? 2 : 1);
       mbar_init(fwd_ready + s, 1);
       mbar_init(fwd_ready + kStages + s, 1);
     }
@@ -533,8 +533,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           }
           if (lane == 0) {
             mbar_wait(p, empty + stage, phase ^ 1);
-            // Stages the forwarder will not touch: arrive on its behalf (empty counts 2).
-            if (fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
+            // gather_b: stages the forwarder will not touch are arrived on its behalf (empty
+            // counts 2); the A-carrying AG forwards from global memory and never holds a stage.
+            if (kGatherB && fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
             uint8_t* sa = smem_a + stage * kAStageBytes;
             uint8_t* sb = smem_b + stage * kBStageBytes;
             const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
@@ -596,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           tc_fence_after();
           const uint32_t d = tmem_base + a * BN;
           int fwd_nt = -1;
-          if (fwd) {
+          if (fwd && kGatherB) {
             const Tile t = get_tile(p, lin, 0);
             const int it = t.step % p.T;
             const int key = kGatherB ? t.pair : t.nt;
@@ -641,7 +642,98 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       // the warp fences its stores at system scope and publishes the image flags; while one
       // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
       // which keeps the ring's progress argument (step-i images depend only on step i-1).
-      if (fwd) {
+      if (fwd && !kGatherB) {
+        // A-carrying AG: forwarders copy each forwarded image from global memory -- step 0
+        // from x (row-major, swizzled here into the SW128 image layout, zero past K), step
+        // i > 0 from the inbox image of slot i-1 once the predecessor's flag is seen -- into
+        // the successor's slot. They never hold a pipeline stage (gating stage reuse on the
+        // forwarder cost 10-18 us per call at TP = 8) and depend only on earlier steps'
+        // images, so the ring progresses independently of the GEMM. Two warps alternate
+        // batches; each fences and publishes its batch's flags.
+        const int grp = warp - 2;
+        // unpublished images of the current tile (flags are always published by tile end)
+        int unpub[8];  // fbatch <= 8 on this path
+        int nunpub = 0;
+        int fo = 0;
+        int cur_slot = 0, cur_dst = 0;
+        auto flush = [&]() {
+          const uint64_t tf0 = p.trace ? globaltimer() : 0;
+          fence_sys();
+          __syncwarp();
+          if (lane == 0 && rank != p.fault_rank)
+            for (int i = 0; i < nunpub; ++i) st_relaxed_sys(flag_ptr(p, par, cur_dst, cur_slot, unpub[i]), ep);
+          if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
+          nunpub = 0;
+        };
+        const char* xh = p.x + h * p.x_rank_stride;
+        for (int lin = gp; lin < ntiles; lin += GP) {
+          const Tile t = get_tile(p, lin, cta);
+          const int pass = t.step / p.T, it = t.step - pass * p.T;
+          const int key = t.nt;
+          if (!(it < p.T - 1 && key < nfwd)) continue;
+          const int slot = pass * (p.T - 1) + it;
+          const int dst_rank = p.sched[rank][it][0];
+          cur_slot = slot;
+          cur_dst = dst_rank;
+          const uint64_t t0 = p.trace ? globaltimer() : 0;
+          const bool live = t.valid > 0;
+          const int64_t img0 = static_cast<int64_t>(t.mb) * p.nkb;
+          const char* xrow0 = xh + ((static_cast<int64_t>(t.b) * p.x_rows + pass * p.Sc + t.row0) * p.K) * 2;
+          for (int kb = key; kb < p.nkb; kb += nfwd) {
+            const bool mine = ((fo / fbatch) & 1) == grp;
+            const bool batch_end = (fo % fbatch) == fbatch - 1;
+            ++fo;
+            if (!mine) continue;
+            if (live) {
+              const int64_t img = img0 + kb;
+              char* dst = slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes;
+              if (it == 0) {
+                // 16-B chunk idx = row * 8 + c of the 128 x 128 B image; SW128: chunk c of
+                // row r sits at r * 128 + ((c ^ (r & 7)) << 4)
+                // lane owns chunk c = lane & 7 of rows (lane >> 3) + 4 * i: one column per lane
+                const int c = lane & 7, r0 = lane >> 3;
+                const int64_t col = static_cast<int64_t>(kb) * BK + c * 8;
+                const bool col_ok = col < p.K;
+                const char* xs = xrow0 + (static_cast<int64_t>(r0) * p.K + col) * 2;
+                const int64_t xstep = static_cast<int64_t>(4) * p.K * 2;  // 4 rows
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint4 v[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) {
+                    const int r = r0 + 4 * (q * 8 + i);
+                    v[i] = (col_ok && r < t.valid) ? *reinterpret_cast<const uint4*>(xs + (q * 8 + i) * xstep)
+                                                   : make_uint4(0u, 0u, 0u, 0u);
+                  }
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) {
+                    const int r = r0 + 4 * (q * 8 + i);
+                    *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) << 4)) = v[i];
+                  }
+                }
+              } else {
+                const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
+                if (lane == 0) wait_flag(p, fsrc, rank, t.step, lin, ep);
+                __syncwarp();
+                (void)ld_acquire_sys(fsrc);  // every lane reads the image after the flag
+                const uint4* src = reinterpret_cast<const uint4*>(slot_ptr(p, par, rank, slot - 1) + img * kAStageBytes);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  uint4 v[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) v[i] = src[(q * 8 + i) * 32 + lane];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(dst)[(q * 8 + i) * 32 + lane] = v[i];
+                }
+              }
+              unpub[nunpub++] = static_cast<int>(img);
+            }
+            if (batch_end && nunpub > 0) flush();
+          }
+          if (nunpub > 0) flush();
+          if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
+        }
+      } else if (fwd) {
         const int grp = warp - 2;
         uint32_t* unpub[16];
         int nunpub = 0;

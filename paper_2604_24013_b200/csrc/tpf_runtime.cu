@@ -558,8 +558,11 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
 
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
   // Performance-only: rank 0 of a `world`-rank group on this GPU, with every peer virtual.
-  // Peer heaps alias one scratch heap (sends land there), and this rank's flag blocks are
-  // pre-set to 0xFFFFFFFF, so every peer wait passes at once and wire / inbox data is stale.
+  // Peer heaps alias this rank's own heap, so a send lands in this rank's inbox slot of the
+  // same index -- the slot the real successor would fill -- and is read back one step later
+  // while still L2-resident, as data arriving over NVLink would be. This rank's flag blocks
+  // are pre-set to 0xFFFFFFFF (sends write the call's epoch, which still passes), so every
+  // peer wait passes at once and wire / inbox contents are stale.
   // The kernels run the real protocol instructions at full-GPU scale, which measures what one
   // GPU of a TP group computes. Results are NOT meaningful.
   tpf_comm* c = nullptr;
@@ -572,7 +575,7 @@ int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
     tpf_comm_destroy(c);
     return fail(tpf::Status::cuda(std::string("tpf_comm_create_virtual: ") + cudaGetErrorString(e)));
   }
-  for (int r = 1; r < world; ++r) c->sym[r] = c->virtual_peers;
+  for (int r = 1; r < world; ++r) c->sym[r] = c->local;
   c->peers_ready = true;
   *out = c;
   return TPF_OK;
