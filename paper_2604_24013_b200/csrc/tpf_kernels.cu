@@ -808,11 +808,13 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     const int64_t tile_bytes = static_cast<int64_t>(BM) * BN * (p.wire_f32 ? 4 : 2);
     const uint32_t tempty_leader0 = mapa_shared(smem_u32(tempty), 0);
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(tempty + 1), 0);
-    // RS flags are published lazily: one system fence covers the wire stores of up to
-    // kPend tiles, and pending flags are always published before any wait that may block
-    // (an inbox flag, or an accumulator the other group's progress gates), so the ring can
-    // never wait on itself.
-    constexpr int kPend = 2;
+    // RS flags: one system fence covers the wire stores of up to kPend tiles, and pending
+    // flags are always published before any wait that may block (an inbox flag, or an
+    // accumulator the other group's progress gates), so the ring can never wait on itself.
+    // kPend = 1 (publish every tile): at TP = 8 a step is less than one round of pair
+    // tiles, so the successor's next-step tile is often already waiting on this flag; the
+    // lazy kPend = 2 cost 9% on the per-GPU cfg2 GEMM-RS under the self-ring model.
+    constexpr int kPend = 1;
     uint32_t* pend[kPend];
     int npend = 0;
     auto publish = [&]() {
