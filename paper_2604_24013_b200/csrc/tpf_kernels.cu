@@ -643,18 +643,19 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
       // which keeps the ring's progress argument (step-i images depend only on step i-1).
       if (fwd && !kGatherB) {
-        // A-carrying AG: forwarders copy each forwarded image from global memory -- step 0
-        // from x (row-major, swizzled here into the SW128 image layout, zero past K), step
-        // i > 0 from the inbox image of slot i-1 once the predecessor's flag is seen -- into
-        // the successor's slot. They never hold a pipeline stage (gating stage reuse on the
-        // forwarder cost 10-18 us per call at TP = 8) and depend only on earlier steps'
-        // images, so the ring progresses independently of the GEMM. Two warps alternate
-        // batches; each fences and publishes its batch's flags.
-        const int grp = warp - 2;
-        // unpublished images of the current tile (flags are always published by tile end)
-        int unpub[8];  // fbatch <= 8 on this path
+        // A-carrying AG: the ring forward is decoupled from the GEMM. Every CTA's two
+        // forwarder warps take a share of each step's images (round-robin over all CTAs of
+        // the rank), step by step: step 0 copies from x (row-major, swizzled here into the
+        // SW128 image layout, zero past K), step i > 0 copies the inbox image of slot i-1
+        // once the predecessor's flag is seen, into the successor's slot i. No pipeline
+        // stage is ever held (gating stage reuse on a forwarder cost 10-18 us per call at
+        // TP = 8), the work is spread over all SMs, and step i's sends depend only on the
+        // predecessor's step i-1 sends, so the ring runs ahead of the GEMM and cannot wait
+        // on it. Each warp fences and publishes its flags per batch and at every step end.
+        const int fw = g * 2 + (warp - 2);  // this warp's index among the rank's forwarders
+        const int nfw = G * 2;
+        int unpub[8];  // fbatch <= 8
         int nunpub = 0;
-        int fo = 0;
         int cur_slot = 0, cur_dst = 0;
         auto flush = [&]() {
           const uint64_t tf0 = p.trace ? globaltimer() : 0;
@@ -666,35 +667,28 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           nunpub = 0;
         };
         const char* xh = p.x + h * p.x_rank_stride;
-        for (int lin = gp; lin < ntiles; lin += GP) {
-          const Tile t = get_tile(p, lin, cta);
-          const int pass = t.step / p.T, it = t.step - pass * p.T;
-          const int key = t.nt;
-          if (!(it < p.T - 1 && key < nfwd)) continue;
-          const int slot = pass * (p.T - 1) + it;
-          const int dst_rank = p.sched[rank][it][0];
-          cur_slot = slot;
-          cur_dst = dst_rank;
-          const uint64_t t0 = p.trace ? globaltimer() : 0;
-          const bool live = t.valid > 0;
-          const int64_t img0 = static_cast<int64_t>(t.mb) * p.nkb;
-          const char* xrow0 = xh + ((static_cast<int64_t>(t.b) * p.x_rows + pass * p.Sc + t.row0) * p.K) * 2;
-          for (int kb = key; kb < p.nkb; kb += nfwd) {
-            const bool mine = ((fo / fbatch) & 1) == grp;
-            const bool batch_end = (fo % fbatch) == fbatch - 1;
-            ++fo;
-            if (!mine) continue;
-            if (live) {
-              const int64_t img = img0 + kb;
-              char* dst = slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes;
+        const int nimg = p.nmb * p.nkb;
+        for (int pass = 0; pass < p.m; ++pass) {
+          for (int it = 0; it < p.T - 1; ++it) {
+            const int slot = pass * (p.T - 1) + it;
+            cur_slot = slot;
+            cur_dst = p.sched[rank][it][0];
+            const uint64_t t0 = p.trace ? globaltimer() : 0;
+            for (int img = fw; img < nimg; img += nfw) {
+              const int mb = img / p.nkb, kb = img - mb * p.nkb;
+              const int bb = mb / p.nmb_per_batch, j = mb - bb * p.nmb_per_batch;
+              const int row0 = j * BM;
+              const int valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - row0));
+              if (valid <= 0) continue;  // padding m-block of an odd pair: never read
+              char* dst = slot_ptr(p, par, cur_dst, slot) + static_cast<int64_t>(img) * kAStageBytes;
               if (it == 0) {
-                // 16-B chunk idx = row * 8 + c of the 128 x 128 B image; SW128: chunk c of
-                // row r sits at r * 128 + ((c ^ (r & 7)) << 4)
-                // lane owns chunk c = lane & 7 of rows (lane >> 3) + 4 * i: one column per lane
+                // lane owns 16-B chunk c = lane & 7 of rows (lane >> 3) + 4 * i; SW128: chunk c
+                // of row r sits at r * 128 + ((c ^ (r & 7)) << 4)
                 const int c = lane & 7, r0 = lane >> 3;
                 const int64_t col = static_cast<int64_t>(kb) * BK + c * 8;
                 const bool col_ok = col < p.K;
-                const char* xs = xrow0 + (static_cast<int64_t>(r0) * p.K + col) * 2;
+                const char* xs =
+                    xh + ((static_cast<int64_t>(bb) * p.x_rows + pass * p.Sc + row0 + r0) * p.K + col) * 2;
                 const int64_t xstep = static_cast<int64_t>(4) * p.K * 2;  // 4 rows
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -702,8 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 #pragma unroll
                   for (int i = 0; i < 8; ++i) {
                     const int r = r0 + 4 * (q * 8 + i);
-                    v[i] = (col_ok && r < t.valid) ? *reinterpret_cast<const uint4*>(xs + (q * 8 + i) * xstep)
-                                                   : make_uint4(0u, 0u, 0u, 0u);
+                    v[i] = (col_ok && r < valid) ? *reinterpret_cast<const uint4*>(xs + (q * 8 + i) * xstep)
+                                                 : make_uint4(0u, 0u, 0u, 0u);
                   }
 #pragma unroll
                   for (int i = 0; i < 8; ++i) {
@@ -713,10 +707,11 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                 }
               } else {
                 const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
-                if (lane == 0) wait_flag(p, fsrc, rank, t.step, lin, ep);
+                if (lane == 0) wait_flag(p, fsrc, rank, pass * p.T + it, img, ep);
                 __syncwarp();
                 (void)ld_acquire_sys(fsrc);  // every lane reads the image after the flag
-                const uint4* src = reinterpret_cast<const uint4*>(slot_ptr(p, par, rank, slot - 1) + img * kAStageBytes);
+                const uint4* src =
+                    reinterpret_cast<const uint4*>(slot_ptr(p, par, rank, slot - 1) + static_cast<int64_t>(img) * kAStageBytes);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   uint4 v[8];
@@ -726,12 +721,12 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                   for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(dst)[(q * 8 + i) * 32 + lane] = v[i];
                 }
               }
-              unpub[nunpub++] = static_cast<int>(img);
+              unpub[nunpub++] = img;
+              if (nunpub == fbatch) flush();
             }
-            if (batch_end && nunpub > 0) flush();
+            if (nunpub > 0) flush();
+            if (p.trace && lane == 0) trace_rec(p, TR_AG_PIECE, rank, slot, fw, t0, globaltimer());
           }
-          if (nunpub > 0) flush();
-          if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
         }
       } else if (fwd) {
         const int grp = warp - 2;
