@@ -428,8 +428,10 @@ def run_ours(args, rank, world, local_rank):
 
 
 def virtual_block(args, dev, stream, T):
-    """One GPU of a real TP=T group at full scale: rank 0 with virtual peers (every peer wait
-    passes at once, sends land in a scratch heap) runs the cfg2 block's per-rank AG-GEMM +
+    """One GPU of a real TP=T group at full scale: rank 0 with virtual peers (a self-ring: the
+    peers alias this rank's heap, so every send fills the slot this rank reads one step later
+    and the ring's step-to-step dependencies are real, with zero link latency) runs the cfg2
+    block's per-rank AG-GEMM +
     SwiGLU and GEMM-RS with the whole protocol. Against compute-only mode this is the
     protocol's on-GPU cost per GPU; NVLink latency is the part it cannot show."""
     import statistics
@@ -481,8 +483,9 @@ def virtual_block(args, dev, stream, T):
     wire = (T - 1) / T * SEQ * 2
     t_roof_ag = max(fl_ag / pk, wire * D_MODEL / 900e9) * 1e3
     t_roof_rs = max(fl_rs / pk, wire * D_MODEL / 900e9) * 1e3
-    return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (waits pass at "
-                             "once, sends land in a local scratch heap); medians of 5 rounds of 20 "
+    return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (self-ring: "
+                             "peers alias the own heap, sends fill the slot read one step later, zero link "
+                             "latency); medians of 5 rounds of 20 "
                              "back-to-back calls per op",
             "ag_gemm_ms": m["ag"], "gemm_rs_ms": m["rs"], "compute_only_ag_ms": m["ag_co"],
             "compute_only_rs_ms": m["rs_co"],

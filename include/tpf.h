@@ -92,10 +92,12 @@ int tpf_comm_open_peers(tpf_comm* c, const void* handles /* world * TPF_IPC_HAND
  * out[world][...]. */
 int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm** out);
 
-/* Performance-only: rank 0 of a `world`-rank group whose peers are virtual (their heaps alias
- * one scratch buffer, this rank's flags are pre-set so every peer wait passes immediately).
- * Runs the full per-rank protocol at full-GPU scale -- what one GPU of a TP group computes --
- * but the results are meaningless. For measurement tools only. */
+/* Performance-only: rank 0 of a `world`-rank group whose peers are virtual: their heaps
+ * alias this rank's own heap (a self-ring), so each send fills the slot this rank reads one
+ * step later and the ring's step-to-step waits are real, with zero link latency (the flags
+ * start pre-set, so the first call after creation does not wait). Runs the full per-rank
+ * protocol at full-GPU scale -- what one GPU of a TP group computes -- but the results are
+ * meaningless. For measurement tools only. */
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out);
 int tpf_comm_destroy(tpf_comm* c);
 int tpf_comm_rank(const tpf_comm* c);

@@ -201,9 +201,10 @@ class Communicator:
 
     @classmethod
     def virtual_group(cls, world: int, sym_bytes: int) -> "Communicator":
-        """Performance-only: rank 0 of a `world`-rank group with virtual peers (every peer wait
-        passes at once, wire data is stale). Per-rank tensors, full-GPU scale; results are
-        meaningless. See tpf_comm_create_virtual."""
+        """Performance-only: rank 0 of a `world`-rank group with virtual peers. The peers alias
+        this rank's own heap (a self-ring): each send fills the slot this rank reads one step
+        later, so the ring's step-to-step waits are real (zero link latency). Per-rank
+        tensors, full-GPU scale; results are meaningless. See tpf_comm_create_virtual."""
         h = C.c_void_p()
         _check(_lib.tpf_comm_create_virtual(world, sym_bytes, C.byref(h)))
         return cls(h.value, 0, world, False)
