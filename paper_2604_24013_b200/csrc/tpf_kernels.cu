@@ -6,24 +6,25 @@
 //   OP_AG  decomposed all-gather + GEMM (fuse_all_gather + column_parallel_forward,
 //          reference collectives.cpp:237-279, layers.cpp:120-127).
 //
-// CTA pairs (cluster of 2, tcgen05 cta_group::2), one CTA per SM, 8 warps each:
+// CTA pairs (cluster of 2, tcgen05 cta_group::2), one CTA per SM, 12 warps each:
 //   warp 0      TMA producer: this CTA's 128-row A block (tensor map or AG wire image)
 //               and its half of the 256-column B tile; completion lands on the leader's
 //               full barrier
 //   warp 1      (leader CTA only) tcgen05.mma.cta_group::2, 256x256x16 bf16 -> fp32, two
 //               TMEM accumulators; commits multicast to both CTAs' barriers
-//   warp 2      TMEM allocator; AG ring forwarder: bulk-stores each landed A stage (already
-//               the SWIZZLE_128B operand image) from SMEM to the successor's slot over NVLink
-//   warps 4-7   epilogue: tcgen05.ld of this CTA's 128 rows -> (+ inbox) -> peer / output
-//
+//   warps 2-3   TMEM allocator (warp 2); AG ring forwarders: copy a share of every step's
+//               wire images from global memory (x at step 0, the inbox after its flag
+//               later) to the successor's slot over NVLink, independent of the GEMM
+//   warps 4-11  two epilogue warpgroups, one per TMEM accumulator: tcgen05.ld of this
+//               CTA's 128 rows -> (+ inbox) -> peer / output
 // Work is a static, iteration-major tile list (step = pass * T + iteration), so every
 // cross-rank dependency points to an earlier step and the persistent grid always makes
 // progress. Wire formats are chosen so the consumer does no re-layout:
 //   RS wire  = the TMEM 32x32b fragment image (thread-row interleaved by 16 B column
 //              groups), so each warp-wide 16 B store/load touches 512 contiguous bytes;
 //   AG wire  = the SWIZZLE_128B K-major UMMA operand image of a 128x64 A tile (16 KiB):
-//              exactly the bytes of the sender's pipeline stage, so forwarding is one
-//              SMEM->peer bulk store and the receiver TMA-loads it straight into a stage.
+//              exactly the bytes of a pipeline stage, so the receiver TMA-loads it
+//              straight into a stage and forwarding it onwards is a verbatim copy.
 // Flags carry the per-call epoch (monotonic, never reset); slots are double-buffered by
 // epoch parity. Every spin is bounded by a %globaltimer deadline and reports into a
 // device error record instead of trapping.
@@ -634,14 +635,6 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       }
     } else {
       // ===================================================== AG ring forwarders (warps 2-3)
-      // Forwarded stage uses (tile nt < nfwd, k-block kb % nfwd == nt) are split into batches
-      // of fbatch alternating between the two warps. For each of its uses a warp waits on its
-      // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B A image out of SMEM
-      // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4 into
-      // the successor's slot (NVLink peer stores). At the end of its batch (and of every tile)
-      // the warp fences its stores at system scope and publishes the image flags; while one
-      // warp fences, the other copies. Flags never stay unpublished across a tile boundary,
-      // which keeps the ring's progress argument (step-i images depend only on step i-1).
       if (fwd && !kGatherB) {
         // A-carrying AG: the ring forward is decoupled from the GEMM. Every CTA's two
         // forwarder warps take a share of each step's images (round-robin over all CTAs of
@@ -729,6 +722,14 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
           }
         }
       } else if (fwd) {
+        // DP parameter all-gather (gather_b: the ring carries weight row blocks): forwarded
+        // stage uses (tile pair < nfwd, k-block kb % nfwd == pair) are split into batches of
+        // fbatch alternating between the two warps. For each of its uses a warp waits on its
+        // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B image out of SMEM
+        // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4
+        // into the successor's slot. At the end of its batch (and of every tile) the warp
+        // fences its stores at system scope and publishes the image flags. Flags never stay
+        // unpublished across a tile boundary (step-i images depend only on step i-1).
         const int grp = warp - 2;
         uint32_t* unpub[16];
         int nunpub = 0;
