@@ -38,6 +38,9 @@ for cfg, S, K_ag, N_ag, K_rs, N_rs in (("cfg2", 8192, 4096, 28672, 14336, 4096),
                                                  tpf.sym_bytes_rs(T, 1, S, K_rs // T, N_rs, 1, tpf.BF16)))
     res[cfg + "_ag"] = loop(lambda: comm.ag_gemm(x, w, y))
     res[cfg + "_rs"] = loop(lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16))
+    if T % 2 == 0:
+        res[cfg + "_rs_pw"] = loop(lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.PAIRWISE, wire=tpf.BF16))
+    res[cfg + "_rs_circ"] = loop(lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.CIRCULAR, wire=tpf.BF16))
     res[cfg + "_ag_gemm"] = loop(lambda: tpf.gemm(xg, w, yg))
     comm.set_compute_only(True)
     res[cfg + "_ag_co"] = loop(lambda: comm.ag_gemm(x, w, y))
