@@ -253,9 +253,9 @@ __device__ __forceinline__ void direct_fold(const KParams& p, const char* slot0,
 }  // namespace
 
 // rs_direct last step: fold the T-1 received partials into the own one, sub-chunk by
-// sub-chunk. Not inlined: its T-1 in-flight inbox loads per sub-chunk would otherwise add
-// to the register pressure of the pipelined epilogue and make the kernel spill.
-__device__ __noinline__ void rs_epilogue_fold(const KParams& p, uint32_t taddr, const char* in0, char* rp,
+// sub-chunk. Inlined: with the epilogue warpgroups at 208 registers it fits without spills,
+// and the ABI call of a non-inlined version cost 11% on the per-GPU pairwise GEMM-RS.
+__device__ __forceinline__ void rs_epilogue_fold(const KParams& p, uint32_t taddr, const char* in0, char* rp,
                                               int64_t ocol0, int row, bool valid, uint32_t tempty_a) {
   for (int j = 0; j < BN / 32; ++j) {
     uint32_t r[32];
