@@ -352,13 +352,26 @@ def run_ours(args, rank, world, local_rank):
         base_ms = None
         print(f"[bench] baseline failed: {exc}", file=sys.stderr)
 
-    # ---- single-GPU emulation of TP=8 (one persistent launch hosts all 8 ranks)
-    emu = None
-    if world == 1 and args.emulate_tp > 1:
-        emu = emulated_block(args, dev, stream, args.emulate_tp)
+    # ---- CPU reference sample (rank 0 at N = 1). It runs before the per-GPU blocks below, so
+    # the GPU idles ~10 s after the sustained bench load and those blocks start cool.
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        nproc = os.cpu_count() or 1
+        cbs = cpu_reference_sample(max(1, min(8, nproc)), 8)
+        cb = cbs[0] if cbs else None
+        if cb:
+            cpu = {"value": cb["tflops"], "unit": "TFLOP/s", "cores": cb["ranks"], "kind": "reference",
+                   "sample": f"{cb['tokens']} tokens of the block ({cb['ranks']} simulated TP ranks, "
+                             f"one thread each), {cb['seconds']:.1f} s of reference CPU work, host nproc={nproc}"}
+
+    # ---- one GPU of a TP=8 group at full scale (virtual peers), then the single-GPU
+    # emulation of TP=8 (one persistent launch hosts all 8 ranks)
     virt = None
     if world == 1 and args.emulate_tp > 1:
         virt = virtual_block(args, dev, stream, args.emulate_tp)
+    emu = None
+    if world == 1 and args.emulate_tp > 1:
+        emu = emulated_block(args, dev, stream, args.emulate_tp)
 
     if rank != 0:
         return
@@ -370,15 +383,6 @@ def run_ours(args, rank, world, local_rank):
     if os.path.exists(tpath):
         with open(tpath) as f:
             traffic = json.load(f).get(f"ag_gemm_tp{T}")
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        nproc = os.cpu_count() or 1
-        cbs = cpu_reference_sample(max(1, min(8, nproc)), 8)
-        cb = cbs[0] if cbs else None
-        if cb:
-            cpu = {"value": cb["tflops"], "unit": "TFLOP/s", "cores": cb["ranks"], "kind": "reference",
-                   "sample": f"{cb['tokens']} tokens of the block ({cb['ranks']} simulated TP ranks, "
-                             f"one thread each), {cb['seconds']:.1f} s of reference CPU work, host nproc={nproc}"}
     out = {
         "metric": METRIC,
         "value": value,
