@@ -520,37 +520,41 @@ def emulated_block(args, dev, stream, T):
         comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
         comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
 
+    import statistics
+
     for _ in range(args.warmup):
         step()
     comm.sync(stream)
-    n = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
-    for i in range(n):
-        ev[i][0].record(stream)
-        comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
-        ev[i][1].record(stream)
-        comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
-        ev[i][2].record(stream)
+
+    def timed(k):
+        # k back-to-back steps, per-op events on the launch stream
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(k)]
+        for i in range(k):
+            ev[i][0].record(stream)
+            comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
+            ev[i][1].record(stream)
+            comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
+            ev[i][2].record(stream)
+        torch.cuda.synchronize(dev)
+        return (ev[0][0].elapsed_time(ev[-1][2]) / k, sum(e[0].elapsed_time(e[1]) for e in ev) / k,
+                sum(e[1].elapsed_time(e[2]) for e in ev) / k)
+
+    # fused and compute-only rounds alternate (medians), so both see the same power state
+    k = max(3, min(args.steps, 10))
+    fused, conly = [], []
+    for _ in range(5):
+        comm.set_compute_only(False)
+        fused.append(timed(k))
+        comm.set_compute_only(True)
+        conly.append(timed(k))
+    comm.set_compute_only(False)
     comm.sync(stream)
-    total = ev[0][0].elapsed_time(ev[-1][2]) / n
-    ag = sum(e[0].elapsed_time(e[1]) for e in ev) / n
-    rs = sum(e[1].elapsed_time(e[2]) for e in ev) / n
-    comm.set_compute_only(True)
-    for _ in range(2):
-        step()
-    torch.cuda.synchronize(dev)
-    for i in range(n):
-        ev[i][0].record(stream)
-        comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
-        ev[i][1].record(stream)
-        comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
-        ev[i][2].record(stream)
-    comm.sync(stream)
-    c_ag = sum(e[0].elapsed_time(e[1]) for e in ev) / n
-    c_rs = sum(e[1].elapsed_time(e[2]) for e in ev) / n
+    total, ag, rs = (statistics.median(c) for c in zip(*fused))
+    _, c_ag, c_rs = (statistics.median(c) for c in zip(*conly))
     comm.close()
     return {"tp": T, "note": "all ranks on ONE GPU (local group, each rank on 148/T SMs); wire traffic "
-                             "goes through local HBM, not NVLink",
+                             "goes through local HBM, not NVLink; medians of 5 alternating fused / "
+                             "compute-only rounds",
             "ms_per_step": total, "tflops": block_flops(SEQ) / (total * 1e-3) / 1e12,
             "ag_gemm_ms": ag, "gemm_rs_ms": rs, "compute_only_ag_ms": c_ag, "compute_only_rs_ms": c_rs,
             "exposed_comm_us": {"ag": 1e3 * (ag - c_ag), "rs": 1e3 * (rs - c_rs),
