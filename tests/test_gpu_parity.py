@@ -934,8 +934,9 @@ def test_ulysses_and_query_split_batch2():
 
 
 def test_virtual_group_runs_every_operator():
-    """The performance-only virtual group runs each fused operator to completion (no waits
-    can block: peer flags are pre-set) and leaves the communicator usable."""
+    """The performance-only virtual group (a self-ring: the peers alias this rank's heap, so
+    every wait is satisfied by this rank's own earlier send of the same call) runs each fused
+    operator to completion, repeatedly, and leaves the communicator usable."""
     T, S, D, H = 8, 1024, 256, 1024
     comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, D, H // T),
                                                  tpf.sym_bytes_rs(T, 1, S, H // T, D, 1),
