@@ -99,9 +99,28 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
  * protocol at full-GPU scale -- what one GPU of a TP group computes -- but the results are
  * meaningless. For measurement tools only. */
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out);
+/* Split group: `world` communicators on the current GPU, one per rank, each with its own
+ * symmetric heap, device epoch and error record -- tpf_comm_create's per-process
+ * communicator, with the other ranks' heaps mapped directly instead of through CUDA IPC.
+ * Every fused GEMM call (tpf_ag_gemm, tpf_gemm_rs, tpf_dp_grad_rs, tpf_dp_param_ag_gemm) on
+ * comms[r] builds rank r's launch exactly as the one-process-per-GPU path does (one hosted
+ * rank, rank id r); the launch is deferred until every rank of the group has made the call,
+ * and the last rank's call launches all of them as ONE grid (each rank on 148/world SMs), on
+ * that call's stream. (Ranks whose kernels wait on each other must not be separate launches
+ * on one GPU: nothing makes them co-resident.) Proves the per-rank protocol -- peer stores,
+ * per-rank flags, epochs and waits -- on one GPU. Calls are collective in the reference's
+ * sense (one worker per rank, fabric.hpp:185-226), issued here from one thread in rank order
+ * or from any threads. comms: world pointers, destroyed one by one with tpf_comm_destroy. */
+int tpf_comm_create_split_group(int world, size_t sym_bytes, tpf_comm** comms);
 int tpf_comm_destroy(tpf_comm* c);
 int tpf_comm_rank(const tpf_comm* c);
 int tpf_comm_world(const tpf_comm* c);
+/* The rank that failed, as GroupError::failing_rank() (fabric.hpp:22-31): set by the last
+ * tpf_comm_sync that returned TPF_E_PEER (-1 before). Waiters that give up record the rank
+ * they were blocked on in every rank's blame table; sync follows that chain from the rank
+ * that timed out to a rank that was not blocked (or that failed itself), so the victims of a
+ * failure are not reported in its place. */
+int tpf_comm_failing_rank(const tpf_comm* c);
 /* Synchronise `stream` and check the device error record of every call since
  * the last check. TPF_E_PEER names the failing rank/step via tpf_last_error(). */
 int tpf_comm_sync(tpf_comm* c, void* stream);
@@ -110,7 +129,7 @@ int tpf_comm_sync(tpf_comm* c, void* stream);
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns);
 /* Test hook: rank `rank` (-1 = none) stops publishing its peer flags, as if it
  * had failed mid-collective; its successors time out and tpf_comm_sync reports
- * TPF_E_PEER naming the waiting rank. */
+ * TPF_E_PEER naming `rank` (tpf_comm_failing_rank). */
 int tpf_comm_inject_fault(tpf_comm* c, int rank);
 /* Measurement hook: on != 0 runs the same kernels over the same tile schedule with
  * every peer flag wait, wire store/load and ring forward disabled (results are

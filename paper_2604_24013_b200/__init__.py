@@ -39,7 +39,21 @@ class LogicError(RuntimeError):
 
 
 class GroupError(RuntimeError):
-    """tpfuse::GroupError: a rank failed (here: peer flag wait timed out)."""
+    """tpfuse::GroupError (fabric.hpp:22-31): names the first failing rank. Here a rank fails
+    when it stops delivering its peer flags; the ranks blocked on it (directly or through a
+    chain of waits) time out and follow the blame chain back to it."""
+
+    def __init__(self, msg: str, rank: int = -1):
+        super().__init__(msg)
+        if rank < 0 and msg.startswith("rank "):
+            try:
+                rank = int(msg.split()[1])
+            except ValueError:
+                rank = -1
+        self._rank = rank
+
+    def failing_rank(self) -> int:
+        return self._rank
 
 
 class TpfCudaError(RuntimeError):
@@ -64,6 +78,8 @@ _lib.tpf_schedule_check.argtypes = [C.c_int, C.c_int, _i32p]
 _lib.tpf_comm_create.argtypes = [C.c_int, C.c_int, C.c_size_t, C.POINTER(_vp)]
 _lib.tpf_comm_create_virtual.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
 _lib.tpf_comm_create_local_group.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
+_lib.tpf_comm_create_split_group.argtypes = [C.c_int, C.c_size_t, C.POINTER(_vp)]
+_lib.tpf_comm_failing_rank.argtypes = [_vp]
 _lib.tpf_comm_ipc_handle.argtypes = [_vp, _vp]
 _lib.tpf_comm_open_peers.argtypes = [_vp, _vp]
 _lib.tpf_comm_destroy.argtypes = [_vp]
@@ -103,6 +119,8 @@ EXPORTED_SYMBOLS = (
     "tpf_comm_ipc_handle",
     "tpf_comm_open_peers",
     "tpf_comm_create_local_group",
+    "tpf_comm_create_split_group",
+    "tpf_comm_failing_rank",
     "tpf_comm_destroy",
     "tpf_comm_rank",
     "tpf_comm_world",
@@ -173,6 +191,30 @@ def check_schedule(kind: int, steps) -> None:
     _check(_lib.tpf_schedule_check(kind, n, buf))
 
 
+# ------------------------------------------------------------ argument checks
+# The C ABI takes raw pointers, so every wrapper checks dtype, layout, device and the exact
+# shape of each tensor first and raises ShapeError naming both shapes, as the reference's
+# matmul / accumulate do (tensor.cpp:68-85, 215-221; tensor.hpp:13-16).
+def _require(t, name: str, shape, dtypes=("bf16",), device=None) -> None:
+    import torch
+    names = {"bf16": torch.bfloat16, "f32": torch.float32}
+    if not isinstance(t, torch.Tensor):
+        raise ShapeError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if tuple(t.shape) != tuple(shape):
+        raise ShapeError(f"{name}: shape {tuple(t.shape)} does not match the expected {tuple(shape)}")
+    if t.dtype not in [names[d] for d in dtypes]:
+        raise ShapeError(f"{name}: dtype {t.dtype} not supported (expected {' or '.join(dtypes)})")
+    if not t.is_contiguous():
+        raise ShapeError(f"{name}: tensor must be contiguous (row-major), got strides {tuple(t.stride())}")
+    if device is not None and t.device != device:
+        raise ShapeError(f"{name}: tensor is on {t.device}, the communicator on {device}")
+    elif device is None and t.device.type != "cuda":
+        raise ShapeError(f"{name}: tensor must be on a CUDA device, got {t.device}")
+
+
+OUT_DTYPES = ("bf16", "f32")
+
+
 # --------------------------------------------------------------- communicator
 def _stream_ptr(stream) -> int:
     import torch
@@ -189,15 +231,44 @@ class Communicator:
       handles exchanged with torch.distributed (plumbing only).
     """
 
-    def __init__(self, handle: int, rank: int, world: int, local_group: bool):
+    def __init__(self, handle: int, rank: int, world: int, local_group: bool, device=None):
         self._h = C.c_void_p(handle)
         self.rank, self.world, self.is_local_group = rank, world, local_group
+        if device is None:
+            import torch
+            device = torch.device("cuda", torch.cuda.current_device())
+        self.device = device
+
+    def _lead(self):
+        # local groups take rank-stacked tensors: a leading dim of `world`
+        return (self.world,) if self.is_local_group else ()
+
+    def _dims(self, t, name: str, nd: int):
+        import torch
+        if not isinstance(t, torch.Tensor):
+            raise ShapeError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+        lead = self._lead()
+        if t.dim() != len(lead) + nd or tuple(t.shape[:len(lead)]) != lead:
+            want = "(" + ", ".join([str(w) for w in lead] + ["*"] * nd) + ")"
+            raise ShapeError(f"{name}: shape {tuple(t.shape)} does not match {want}")
+        return tuple(t.shape[len(lead):])
 
     @classmethod
     def local_group(cls, world: int, sym_bytes_per_rank: int) -> "Communicator":
         h = C.c_void_p()
         _check(_lib.tpf_comm_create_local_group(world, sym_bytes_per_rank, C.byref(h)))
         return cls(h.value, 0, world, True)
+
+    @classmethod
+    def split_group(cls, world: int, sym_bytes: int) -> list:
+        """`world` per-rank communicators on the current GPU (tpf_comm_create_split_group):
+        each is a one-process-per-GPU communicator (its own heap, device epoch and error
+        record; per-rank tensors, no stacking) whose peers are the others' heaps. A fused GEMM
+        call on every rank (any order, same stream) runs as one launch once the last rank has
+        made it. Proves the per-rank protocol with real waits on one GPU."""
+        hs = (_vp * world)()
+        _check(_lib.tpf_comm_create_split_group(world, sym_bytes, hs))
+        return [cls(hs[r], r, world, False) for r in range(world)]
 
     @classmethod
     def virtual_group(cls, world: int, sym_bytes: int) -> "Communicator":
@@ -255,8 +326,12 @@ class Communicator:
             _check(_lib.tpf_comm_set_trace(self._h, buf.data_ptr(), buf.numel() // 4 - 1))
 
     def sync(self, stream=None) -> None:
-        """Synchronise the stream and raise GroupError if a peer wait timed out."""
-        _check(_lib.tpf_comm_sync(self._h, _stream_ptr(stream)))
+        """Synchronise the stream and raise GroupError (naming the failing rank, not the
+        rank that timed out) if a peer wait gave up."""
+        rc = _lib.tpf_comm_sync(self._h, _stream_ptr(stream))
+        if rc == E_PEER:
+            raise GroupError(_lib.tpf_last_error().decode(), int(_lib.tpf_comm_failing_rank(self._h)))
+        _check(rc)
 
     def close(self) -> None:
         if self._h:
@@ -275,9 +350,14 @@ class Communicator:
 
         Per rank x: (B, S/T, K) bf16, w: (K, N_local) bf16, out: (B, S, N_local).
         A local group takes rank-stacked tensors (T, ...)."""
-        lead = 1 if self.is_local_group else 0
-        B, sl, K = x.shape[lead:]
-        N = w.shape[-1]
+        B, sl, K = self._dims(x, "ag_gemm x", 3)
+        L, dev = self._lead(), self.device
+        N = self._dims(w, "ag_gemm w", 2)[1]
+        _require(x, "ag_gemm x", L + (B, sl, K), device=dev)
+        _require(w, "ag_gemm w", L + (K, N), device=dev)
+        if m >= 1 and (self.world == 1 or sl % m == 0):  # else the library raises the reference's error
+            _require(out, "ag_gemm out", L + (B, sl * self.world, N // 2 if act == ACT_SWIGLU else N), OUT_DTYPES,
+                     dev)
         _check(_lib.tpf_ag_gemm(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B,
                                 sl * self.world, K, N, m, act, _dtype_code(out), _stream_ptr(stream)))
 
@@ -285,9 +365,13 @@ class Communicator:
         """row_parallel_forward / fuse_reduce_scatter (layers.cpp:129-138).
 
         Per rank x: (B, S, K_local) bf16, w: (K_local, N) bf16, out: (B, S/T, N)."""
-        lead = 1 if self.is_local_group else 0
-        B, S, K = x.shape[lead:]
-        N = w.shape[-1]
+        B, S, K = self._dims(x, "gemm_rs x", 3)
+        L, dev = self._lead(), self.device
+        N = self._dims(w, "gemm_rs w", 2)[1]
+        _require(x, "gemm_rs x", L + (B, S, K), device=dev)
+        _require(w, "gemm_rs w", L + (K, N), device=dev)
+        if m >= 1 and S % (self.world * m) == 0:  # else the library raises the reference's error
+            _require(out, "gemm_rs out", L + (B, S // self.world, N), OUT_DTYPES, dev)
         _check(_lib.tpf_gemm_rs(self._h, x.data_ptr(), w.data_ptr(), out.data_ptr(), B, S, K, N,
                                 kind, m, wire, _dtype_code(out), _stream_ptr(stream)))
 
@@ -295,8 +379,13 @@ class Communicator:
         """DP gradient reduce-scatter fused into the weight-gradient GEMM (cfg 4):
         dW_r = rows [r*K/T, (r+1)*K/T) of sum_q X_q^T dY_q. Per rank X: (M_local, K), dY: (M_local, N),
         dW: (K/T, N); a local group takes rank-stacked tensors."""
-        M_local, K = X.shape[-2:]
-        N = dY.shape[-1]
+        M_local, K = self._dims(X, "dp_grad_rs X", 2)
+        N = self._dims(dY, "dp_grad_rs dY", 2)[1]
+        L, dev = self._lead(), self.device
+        _require(X, "dp_grad_rs X", L + (M_local, K), device=dev)
+        _require(dY, "dp_grad_rs dY", L + (M_local, N), device=dev)
+        if K % self.world == 0:
+            _require(dW, "dp_grad_rs dW", L + (K // self.world, N), OUT_DTYPES, dev)
         _check(_lib.tpf_dp_grad_rs(self._h, X.data_ptr(), dY.data_ptr(), dW.data_ptr(), M_local, K, N, kind, m,
                                    wire, _dtype_code(dW), _stream_ptr(stream)))
 
@@ -304,8 +393,12 @@ class Communicator:
         """DP parameter all-gather fused into the forward GEMM (cfg 4, a19): out = x . W^T where
         W (N x K) is row-sharded over the ranks (PyTorch Linear layout). Per rank x: (M_local, K),
         w_rows: (N/T, K), out: (M_local, N); a local group takes rank-stacked tensors."""
-        M_local, K = x.shape[-2:]
-        N_local = w_rows.shape[-2]
+        M_local, K = self._dims(x, "dp_param_ag_gemm x", 2)
+        N_local = self._dims(w_rows, "dp_param_ag_gemm w_rows", 2)[0]
+        L, dev = self._lead(), self.device
+        _require(x, "dp_param_ag_gemm x", L + (M_local, K), device=dev)
+        _require(w_rows, "dp_param_ag_gemm w_rows", L + (N_local, K), device=dev)
+        _require(out, "dp_param_ag_gemm out", L + (M_local, self.world * N_local), OUT_DTYPES, dev)
         _check(_lib.tpf_dp_param_ag_gemm(self._h, x.data_ptr(), w_rows.data_ptr(), out.data_ptr(), M_local, K,
                                          N_local, _dtype_code(out), _stream_ptr(stream)))
 
@@ -313,7 +406,14 @@ class Communicator:
         """fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218; BASELINE cfg 5).
         Per rank q/k/v: (batch*heads, S, Dh) bf16; out: (batch, S/T, T*heads*Dh) bf16.
         A local group takes rank-stacked tensors."""
-        S, Dh = q.shape[-2:]
+        G, S, Dh = self._dims(q, "attention_a2a q", 3)
+        L, dev, T = self._lead(), self.device, self.world
+        if G != batch * heads:
+            raise ShapeError(f"attention_a2a q: {G} head rows != batch {batch} x heads {heads}")
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _require(t, f"attention_a2a {name}", L + (G, S, Dh), device=dev)
+        if S % T == 0:
+            _require(out, "attention_a2a out", L + (batch, S // T, T * heads * Dh), ("bf16",), dev)
         _check(_lib.tpf_attention_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch, heads,
                                       S, Dh, int(bool(scale)), _stream_ptr(stream)))
 
@@ -321,8 +421,16 @@ class Communicator:
                                wire: int = F32, scale: bool = True, stream=None) -> None:
         """query_split_attention (Alg. 4, layers.cpp:149-172). Per rank q/k/v: (batch*heads, S, 128)
         bf16, w_o: (heads*128, D) bf16 (row shard), out: (batch, S/T, D). Local groups: rank-stacked."""
-        S, Dh = q.shape[-2:]
-        D = w_o.shape[-1]
+        G, S, Dh = self._dims(q, "query_split_attention q", 3)
+        D = self._dims(w_o, "query_split_attention w_o", 2)[1]
+        L, dev, T = self._lead(), self.device, self.world
+        if G != batch * heads:
+            raise ShapeError(f"query_split_attention q: {G} head rows != batch {batch} x heads {heads}")
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _require(t, f"query_split_attention {name}", L + (G, S, Dh), device=dev)
+        _require(w_o, "query_split_attention w_o", L + (heads * Dh, D), device=dev)
+        if S % T == 0:
+            _require(out, "query_split_attention out", L + (batch, S // T, D), OUT_DTYPES, dev)
         _check(_lib.tpf_query_split_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), w_o.data_ptr(),
                                               out.data_ptr(), batch, heads, S, Dh, D, kind, wire, _dtype_code(out),
                                               int(bool(scale)), _stream_ptr(stream)))
@@ -331,7 +439,15 @@ class Communicator:
         """Ulysses first all-to-all (ref_all_to_all of layers_test.cpp:347-397):
         per rank q/k/v (batch*heads, S/T, Dh) bf16 with every head -> (batch*heads/T, S, Dh), this
         rank's head group over the whole sequence. Local groups: rank-stacked."""
-        sl, Dh = q.shape[-2:]
+        G, sl, Dh = self._dims(q, "ulysses_a2a q", 3)
+        L, dev, T = self._lead(), self.device, self.world
+        if G != batch * heads:
+            raise ShapeError(f"ulysses_a2a q: {G} head rows != batch {batch} x heads {heads}")
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _require(t, f"ulysses_a2a {name}", L + (G, sl, Dh), device=dev)
+        if heads % T == 0:
+            for name, t in (("q_out", q_out), ("k_out", k_out), ("v_out", v_out)):
+                _require(t, f"ulysses_a2a {name}", L + (batch * heads // T, sl * T, Dh), ("bf16",), dev)
         _check(_lib.tpf_ulysses_a2a(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), q_out.data_ptr(),
                                     k_out.data_ptr(), v_out.data_ptr(), batch, heads, sl * self.world, Dh,
                                     _stream_ptr(stream)))
@@ -340,7 +456,13 @@ class Communicator:
         """The whole UP attention (Alg. 5 with its first all-to-all): sequence-sharded q/k/v
         (batch*heads, S/T, 128) per rank -> out (batch, S/T, heads*128), with both all-to-alls fused
         (peer-store inbox + fused flash attention pushing O tiles to the slice owner)."""
-        sl, Dh = q.shape[-2:]
+        G, sl, Dh = self._dims(q, "ulysses_attention q", 3)
+        L, dev = self._lead(), self.device
+        if G != batch * heads:
+            raise ShapeError(f"ulysses_attention q: {G} head rows != batch {batch} x heads {heads}")
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _require(t, f"ulysses_attention {name}", L + (G, sl, Dh), device=dev)
+        _require(out, "ulysses_attention out", L + (batch, sl, heads * Dh), ("bf16",), dev)
         _check(_lib.tpf_ulysses_attention(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), batch,
                                           heads, sl * self.world, Dh, int(bool(scale)), _stream_ptr(stream)))
 
@@ -379,15 +501,24 @@ def _dtype_code(t) -> int:
 
 def gemm(a, b, out, stream=None) -> None:
     """T == 1 degenerate case: out = a @ b on the tcgen05 kernel."""
+    if a.dim() != 2 or b.dim() != 2:
+        raise ShapeError(f"gemm: operands must be 2-D, got {tuple(a.shape)} x {tuple(b.shape)}")
     M, K = a.shape
     N = b.shape[1]
+    if b.shape[0] != K:  # matmul's ShapeError names both shapes (tensor.cpp:68-85)
+        raise ShapeError(f"matmul: shape mismatch {tuple(a.shape)} x {tuple(b.shape)}")
+    _require(a, "gemm a", (M, K))
+    _require(b, "gemm b", (K, N), device=a.device)
+    _require(out, "gemm out", (M, N), OUT_DTYPES, a.device)
     _check(_lib.tpf_gemm(a.data_ptr(), b.data_ptr(), out.data_ptr(), M, K, N, _dtype_code(out),
                          _stream_ptr(stream)))
 
 
 def swiglu(gu, out, stream=None) -> None:
-    rows = gu.numel() // gu.shape[-1]
     F = gu.shape[-1] // 2
+    _require(gu, "swiglu gu", tuple(gu.shape[:-1]) + (2 * F,))
+    _require(out, "swiglu out", tuple(gu.shape[:-1]) + (F,), ("bf16",), gu.device)
+    rows = gu.numel() // gu.shape[-1]
     _check(_lib.tpf_swiglu(gu.data_ptr(), out.data_ptr(), rows, F, _stream_ptr(stream)))
 
 

@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(384, 1) tpf_fmha_a2a_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc<512>(tmem);
-  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, epoch);
+  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, epoch, gridDim.x);
 }
 
 template <bool kQSplit>

@@ -90,19 +90,23 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restri
 }
 
 // Wait until every flag[i] >= epoch (bounded; error record on timeout).
-__global__ void wait_flags_kernel(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns,
-                                  uint32_t* err, int rank) {
+// Wait until every flags[i] >= epoch (bounded; error record + blame entry on give-up). Flag i
+// was written by source rank (first + i) / per_src.
+__device__ __forceinline__ void wait_flag_range(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns,
+                                                uint32_t* err, int rank, const Blame& blame, int64_t first,
+                                                int64_t per_src) {
   const uint64_t t0 = globaltimer();
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     while (ld_relaxed_sys(flags + i) < epoch) {
-      if (ld_relaxed_sys(err + 4)) return;
-      if (globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
-        if (atomicCAS(err, 0u, 1u) == 0u) {
+      const bool abort = ld_relaxed_sys(err + 4) != 0;
+      if (abort || globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
+        if (!abort && atomicCAS(err, 0u, 1u) == 0u) {
           err[1] = static_cast<uint32_t>(rank);
           err[2] = 0xFFFFFFFFu;
           err[3] = static_cast<uint32_t>(i);
         }
+        blame_store(blame.table, blame.T, rank, static_cast<int>((first + i) / per_src));
         atomicExch(err + 4, 1u);
         return;
       }
@@ -112,29 +116,19 @@ __global__ void wait_flags_kernel(const uint32_t* flags, int64_t n, uint32_t epo
   }
 }
 
+__global__ void wait_flags_kernel(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns,
+                                  uint32_t* err, int rank, const __grid_constant__ Blame blame, int64_t first,
+                                  int64_t per_src) {
+  wait_flag_range(flags, n, epoch, timeout_ns, err, rank, blame, first, per_src);
+}
+
 __global__ void wait_flags2_kernel(const uint32_t* flags0, const uint32_t* flags1, int64_t n,
                                    const uint32_t* epoch_dev, uint32_t epoch_static, int64_t timeout_ns,
-                                   uint32_t* err, int rank) {
+                                   uint32_t* err, int rank, const __grid_constant__ Blame blame, int64_t first,
+                                   int64_t per_src) {
   const uint32_t epoch = epoch_dev ? epoch_read(epoch_dev, 0) : epoch_static;
   const uint32_t* flags = (epoch_dev && (epoch & 1u)) ? flags1 : flags0;
-  const uint64_t t0 = globaltimer();
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    while (ld_relaxed_sys(flags + i) < epoch) {
-      if (ld_relaxed_sys(err + 4)) return;
-      if (globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
-        if (atomicCAS(err, 0u, 1u) == 0u) {
-          err[1] = static_cast<uint32_t>(rank);
-          err[2] = 0xFFFFFFFFu;
-          err[3] = static_cast<uint32_t>(i);
-        }
-        atomicExch(err + 4, 1u);
-        return;
-      }
-      __nanosleep(64);
-    }
-    (void)ld_acquire_sys(flags + i);
-  }
+  wait_flag_range(flags, n, epoch, timeout_ns, err, rank, blame, first, per_src);
 }
 
 __global__ void copy_by_parity_kernel(int4* dst, const int4* src0, const int4* src1, int64_t n,
@@ -148,11 +142,13 @@ __global__ void copy_by_parity_kernel(int4* dst, const int4* src0, const int4* s
 }  // namespace
 
 void launch_wait_flags2(const uint32_t* flags0, const uint32_t* flags1, int64_t n, const uint32_t* epoch_dev,
-                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, cudaStream_t st) {
+                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, const Blame& blame,
+                        int64_t first, int64_t per_src, cudaStream_t st) {
   if (n <= 0) return;
   const int threads = 256;
   const int blocks = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 64));
-  wait_flags2_kernel<<<blocks, threads, 0, st>>>(flags0, flags1, n, epoch_dev, epoch, timeout_ns, err, rank);
+  wait_flags2_kernel<<<blocks, threads, 0, st>>>(flags0, flags1, n, epoch_dev, epoch, timeout_ns, err, rank, blame,
+                                                 first, per_src > 0 ? per_src : 1);
 }
 
 void launch_copy_by_parity(void* dst, const void* src0, const void* src1, int64_t bytes, const uint32_t* epoch_dev,
@@ -171,11 +167,12 @@ void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float s
 }
 
 void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
-                       int rank, cudaStream_t st) {
+                       int rank, const Blame& blame, int64_t first, int64_t per_src, cudaStream_t st) {
   if (n <= 0) return;
   const int threads = 256;
   const int blocks = static_cast<int>(std::min<int64_t>((n + threads - 1) / threads, 64));
-  wait_flags_kernel<<<blocks, threads, 0, st>>>(flags, n, epoch, timeout_ns, err, rank);
+  wait_flags_kernel<<<blocks, threads, 0, st>>>(flags, n, epoch, timeout_ns, err, rank, blame, first,
+                                                per_src > 0 ? per_src : 1);
 }
 
 }  // namespace tpf

@@ -36,6 +36,18 @@ enum Mode : int {
                       // a step's tiles wait for their query slice's ready counter (Alg. 4)
 };
 
+// Blame table: a waiter that gives up on a peer flag (timeout, or the group aborting) records
+// the rank it was blocked on, in every rank's table (system-scope stores into the symmetric
+// heaps), so any rank's tpf_comm_sync can follow the chain waiter -> awaited -> ... to the rank
+// that failed -- the reference's GroupError::failing_rank (fabric.hpp:22-31, 207-219), not a
+// victim. Entry [waiter] = awaited + 1; a rank that failed itself (fault injection) stores its
+// own rank + 1. The table sits at the end of the parity-1 flag block.
+constexpr int64_t kBlameBytes = 256;
+struct Blame {
+  uint32_t* table[kMaxRanks];  // every rank's table (peer-mapped); table[0] null: disabled
+  int T;
+};
+
 // Error record in device memory (first error wins).
 //   [0] code (0 ok, 1 peer-flag timeout, 2 mbarrier timeout)
 //   [1] rank  [2] step  [3] tile / piece  [4] abort flag
@@ -105,6 +117,17 @@ struct KParams {
   // Optional device trace (%globaltimer ns): records of 4 x u64 appended via trace[0] counter.
   unsigned long long* trace;
   int64_t trace_cap;  // records
+  Blame blame;
+};
+
+// Split group (tpf_comm_create_split_group): every rank's own per-process launch parameters
+// (n_hosted = 1, rank0 = r, its own heap / epoch / error record), run as ONE launch of
+// n * ctas_per_rank CTAs. Ranks whose kernels wait on each other must never be separate
+// launches on one GPU (nothing makes them co-resident); one launch sized to the resident CTA
+// pairs is.
+struct GroupParams {
+  KParams p[kMaxRanks];
+  int n;
 };
 
 // trace record: {kind | rank << 8 | cta(block) << 16 | step << 32, index, t0, t1}
@@ -158,17 +181,20 @@ struct UlyssesParams {
 
 void launch_ulysses_push(const UlyssesParams& p, cudaStream_t stream);
 cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_fused_group(const GroupParams& gp, int grid, cudaStream_t stream);
 cudaError_t launch_fmha_a2a(const FmhaParams& p, int grid, cudaStream_t stream);
 void launch_softmax(const float* s, void* p, int64_t rows, int64_t cols, float scale, cudaStream_t st);
 // Wait until flags[parity][0..n) >= epoch, epoch / parity read from epoch_dev (the call's
 // current device epoch), or the given static epoch / flags[0] when epoch_dev is null.
+// Flag i of the waited range belongs to source rank (first + i) / per_src (blame on give-up).
 void launch_wait_flags2(const uint32_t* flags0, const uint32_t* flags1, int64_t n, const uint32_t* epoch_dev,
-                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, cudaStream_t st);
+                        uint32_t epoch, int64_t timeout_ns, uint32_t* err, int rank, const Blame& blame,
+                        int64_t first, int64_t per_src, cudaStream_t st);
 // dst <- src[parity of the call's device epoch], `bytes` a multiple of 16.
 void launch_copy_by_parity(void* dst, const void* src0, const void* src1, int64_t bytes, const uint32_t* epoch_dev,
                            cudaStream_t st);
 void launch_wait_flags(const uint32_t* flags, int64_t n, uint32_t epoch, int64_t timeout_ns, uint32_t* err,
-                       int rank, cudaStream_t st);
+                       int rank, const Blame& blame, int64_t first, int64_t per_src, cudaStream_t st);
 int max_pairs();
 int num_sms();
 

@@ -34,6 +34,7 @@
 
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "tpf_internal.h"
 #include "tpf_ptx.cuh"
@@ -106,10 +107,16 @@ __device__ __noinline__ void record_error(const KParams& p, uint32_t code, int r
   atomicExch(p.err + 4, 1u);
 }
 
-// Bounded spin on a peer-written flag (value >= epoch). Returns with acquire
+// A waiter gives up on rank `awaited`: blame entry for the failing-rank chain (tpf::Blame).
+__device__ __noinline__ void give_up(const KParams& p, bool timed_out, int rank, int awaited, int step, int tile) {
+  if (timed_out) record_error(p, 1, rank, step, tile);
+  blame_store(p.blame.table, p.blame.T, rank, awaited);
+}
+
+// Bounded spin on a flag written by rank `awaited` (value >= epoch). Returns with acquire
 // semantics; on timeout / abort returns false (the kernel then drains with garbage
 // and the host raises from the error record).
-__device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, int rank,
+__device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, int rank, int awaited,
                                           int step, int tile, uint32_t epoch) {
   if (ld_relaxed_sys(f) >= epoch) {
     (void)ld_acquire_sys(f);
@@ -125,9 +132,9 @@ __device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, i
       }
       __nanosleep(32);
     }
-    if (aborted(p)) return false;
-    if (globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns)) {
-      record_error(p, 1, rank, step, tile);
+    const bool timed_out = globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns);
+    if (aborted(p) || timed_out) {
+      give_up(p, timed_out && !aborted(p), rank, awaited, step, tile);
       return false;
     }
   }
@@ -354,8 +361,10 @@ __host__ __device__ constexpr bool pdl_instance(int mode) { return mode == MODE_
 
 // Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
 // single-thread producer / MMA loops cost measurable throughput.
+// The kernel body: CTA g of the ctas_per_rank CTAs serving hosted rank h (rank p.rank0 + h).
+// exit_ctas = CTAs that read p's device epoch (the last of them to exit publishes it).
 template <int kOp, int kMode>
-__global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_constant__ KParams p) {
+__device__ __forceinline__ void fused_body(const KParams& p, const int h, const int g, const uint32_t exit_ctas) {
   constexpr bool kAMn = kMode == MODE_DP_GRAD;                         // A MN-major (X^T)
   constexpr bool kGatherB = kMode == MODE_GATHER_B;                    // AG carries B
   constexpr bool kBBatched = kMode == MODE_QK || kMode == MODE_PV;     // B per batch (head)
@@ -382,8 +391,6 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   const int lane = threadIdx.x & 31;
   const int cta = static_cast<int>(cluster_ctarank());
   const bool leader = cta == 0;
-  const int h = blockIdx.x / p.ctas_per_rank;      // hosted rank served by this CTA
-  const int g = blockIdx.x - h * p.ctas_per_rank;  // CTA index within that rank
   const int rank = p.rank0 + h;
   const int G = p.ctas_per_rank;
   const int gp = g >> 1, GP = G >> 1;  // pair index / pairs per rank
@@ -425,6 +432,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
     const uint32_t e = p.epoch_dev ? epoch_read(p.epoch_dev, p.epoch_bump) : p.epoch;
     s_epoch = e;
     s_parity = p.epoch_dev ? static_cast<int>(e & 1u) : p.parity;
+    // fault injection: the failing rank names itself in the blame tables (its successors
+    // time out on its flags and follow the chain to it)
+    if (rank == p.fault_rank && g == 0 && h < p.n_hosted && p.T > 1) blame_store(p.blame.table, p.blame.T, rank, rank);
   }
   tc_fence_before();
   cluster_sync();
@@ -517,9 +527,9 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
               if (poll == 0) tspin = globaltimer();
               __nanosleep(32);
               if ((poll & 255) == 255) {
-                if (aborted(p)) break;
-                if (globaltimer() - tspin > static_cast<uint64_t>(p.timeout_ns)) {
-                  if (lane == 0) record_error(p, 1, rank, t.step, lin);
+                const bool timed_out = globaltimer() - tspin > static_cast<uint64_t>(p.timeout_ns);
+                if (aborted(p) || timed_out) {
+                  if (lane == 0) give_up(p, timed_out && !aborted(p), rank, p.sched[rank][it - 1][1], t.step, lin);
                   break;
                 }
               }
@@ -700,7 +710,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
                 }
               } else {
                 const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
-                if (lane == 0) wait_flag(p, fsrc, rank, pass * p.T + it, img, ep);
+                if (lane == 0) wait_flag(p, fsrc, rank, p.sched[rank][it - 1][1], pass * p.T + it, img, ep);
                 __syncwarp();
                 (void)ld_acquire_sys(fsrc);  // every lane reads the image after the flag
                 const uint4* src =
@@ -894,7 +904,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
         const uint64_t tw0 = (p.trace && lane == 0) ? globaltimer() : 0;
         const uint32_t* fin = flag_ptr(p, par, rank, slot_in, fidx);
         if (npend > 0 && ld_relaxed_sys(fin) < ep) publish();
-        wait_flag(p, fin, rank, t.step, lin, ep);
+        wait_flag(p, fin, rank, p.sched[rank][it - 1][1], t.step, lin, ep);
         if (p.trace && lane == 0 && ew == 0) {
           const uint64_t tw1 = globaltimer();
           if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_IN, rank, t.step, lin, tw0, tw1);
@@ -904,7 +914,8 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
       if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
         publish();
         for (int s = 0; s < p.T - 1; ++s)
-          wait_flag(p, flag_ptr(p, par, rank, pass * (p.T - 1) + s, fidx), rank, t.step, lin, ep);
+          wait_flag(p, flag_ptr(p, par, rank, pass * (p.T - 1) + s, fidx), rank, p.sched[rank][s][1], t.step, lin,
+                    ep);
       }
       __syncwarp();
       char* dst_tile =
@@ -955,7 +966,21 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
   cluster_sync();
   tc_fence_after();
   if (warp == 2) tmem_dealloc_2sm<512>(tmem_base);
-  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, ep);
+  if (threadIdx.x == 0 && p.epoch_dev && p.epoch_bump) epoch_publish(p.epoch_dev, ep, exit_ctas);
+}
+
+template <int kOp, int kMode>
+__global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_constant__ KParams p) {
+  const int h = blockIdx.x / p.ctas_per_rank;  // hosted rank served by this CTA
+  fused_body<kOp, kMode>(p, h, blockIdx.x - h * p.ctas_per_rank, gridDim.x);
+}
+
+// Split group: CTA block r * ctas_per_rank + g runs rank r's own (per-process) parameters.
+template <int kOp, int kMode>
+__global__ void __launch_bounds__(kThreads, 1) tpf_fused_group_kernel(const __grid_constant__ GroupParams gp) {
+  const int r = blockIdx.x / gp.p[0].ctas_per_rank;
+  const KParams& p = gp.p[r];
+  fused_body<kOp, kMode>(p, 0, blockIdx.x - r * p.ctas_per_rank, p.ctas_per_rank);
 }
 
 namespace {
@@ -985,18 +1010,24 @@ int pdl_setting() {
 }
 bool pdl_enabled() { return pdl_setting() != 0; }
 
-template <int kOp, int kMode>
-cudaError_t launch_instance(const KParams& p, int grid, cudaStream_t stream) {
+template <int kOp, int kMode, typename Params>
+cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
+  constexpr bool kGroup = std::is_same<Params, GroupParams>::value;
+  void (*kern)(Params);
+  if constexpr (kGroup)
+    kern = tpf_fused_group_kernel<kOp, kMode>;
+  else
+    kern = tpf_fused_kernel<kOp, kMode>;
   static uint64_t attr_done = 0;
   static bool pool_ok[64];
-  once_per_device(attr_done, [] {
-    cudaFuncSetAttribute(tpf_fused_kernel<kOp, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  once_per_device(attr_done, [kern] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     // the setmaxnreg split must fit the register pool the launch allocates, or
     // setmaxnreg.inc blocks forever
     cudaFuncAttributes fa;
     int dev = 0;
     cudaGetDevice(&dev);
-    pool_ok[dev & 63] = cudaFuncGetAttributes(&fa, tpf_fused_kernel<kOp, kMode>) == cudaSuccess &&
+    pool_ok[dev & 63] = cudaFuncGetAttributes(&fa, kern) == cudaSuccess &&
                         fa.numRegs * kThreads >= 128 * kRegsCtl + 256 * kRegsEpi;
   });
   {
@@ -1019,10 +1050,15 @@ cudaError_t launch_instance(const KParams& p, int grid, cudaStream_t stream) {
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (pdl_instance(kMode) && pdl_enabled()) ? 2 : 1;
-  KParams q = p;
-  q.pdl_trigger = pdl_setting() == 3 ? 0 : pdl_setting();
-  return cudaLaunchKernelEx(&cfg, tpf_fused_kernel<kOp, kMode>, q);
+  if constexpr (kGroup) {
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, p);
+  } else {
+    cfg.numAttrs = (pdl_instance(kMode) && pdl_enabled()) ? 2 : 1;
+    KParams q = p;
+    q.pdl_trigger = pdl_setting() == 3 ? 0 : pdl_setting();
+    return cudaLaunchKernelEx(&cfg, kern, q);
+  }
 }
 
 }  // namespace
@@ -1040,6 +1076,17 @@ cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream) {
     default:
       return p.op == OP_AG ? launch_instance<OP_AG, MODE_STD>(p, grid, stream)
                            : launch_instance<OP_RS, MODE_STD>(p, grid, stream);
+  }
+}
+
+cudaError_t launch_fused_group(const GroupParams& gp, int grid, cudaStream_t stream) {
+  switch (gp.p[0].mode) {
+    case MODE_STD:
+      return gp.p[0].op == OP_AG ? launch_instance<OP_AG, MODE_STD>(gp, grid, stream)
+                                 : launch_instance<OP_RS, MODE_STD>(gp, grid, stream);
+    case MODE_DP_GRAD: return launch_instance<OP_RS, MODE_DP_GRAD>(gp, grid, stream);
+    case MODE_GATHER_B: return launch_instance<OP_AG, MODE_GATHER_B>(gp, grid, stream);
+    default: return cudaErrorInvalidValue;  // other instances are not split-group operations
   }
 }
 

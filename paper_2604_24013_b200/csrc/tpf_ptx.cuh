@@ -123,10 +123,10 @@ __device__ __forceinline__ uint32_t epoch_read(const uint32_t* ep, int bump) {
   asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(ep));
   return v + (bump ? 1u : 0u);
 }
-__device__ __forceinline__ void epoch_publish(uint32_t* ep, uint32_t value) {
-  // one thread per CTA, after the CTA's last use of the epoch
+__device__ __forceinline__ void epoch_publish(uint32_t* ep, uint32_t value, uint32_t ctas) {
+  // one thread per CTA of the `ctas` CTAs that read this epoch, after the CTA's last use of it
   __threadfence();
-  if (atomicAdd(ep + 1, 1u) == gridDim.x - 1) {
+  if (atomicAdd(ep + 1, 1u) == ctas - 1) {
     ep[1] = 0;
     ep[0] = value;
     __threadfence();
@@ -252,6 +252,14 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 }
 
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
+// Blame record (tpf::Blame): entry [waiter] = awaited + 1 in all T ranks' tables. Called by a
+// waiter that gives up on a peer flag; awaited == waiter marks a rank that failed itself.
+__device__ __forceinline__ void blame_store(uint32_t* const* tables, int T, int waiter, int awaited) {
+  if (!tables[0] || waiter < 0 || awaited < 0) return;
+  for (int x = 0; x < T; ++x) st_relaxed_sys(tables[x] + waiter, static_cast<uint32_t>(awaited + 1));
+  fence_sys();
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }

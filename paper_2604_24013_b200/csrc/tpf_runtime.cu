@@ -5,12 +5,15 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tpf.h"
@@ -41,6 +44,9 @@ int fail(const tpf::Status& s) {
   } while (0)
 
 constexpr int64_t kFlagBytesPerParity = 1 << 20;  // 256 Ki flags per parity
+// usable flag bytes per parity: the blame table (tpf::Blame) takes the end of the parity-1 block
+constexpr int64_t kFlagCapBytes = kFlagBytesPerParity - tpf::kBlameBytes;
+constexpr int64_t kBlameOff = 2 * kFlagBytesPerParity - tpf::kBlameBytes;
 constexpr int64_t kDefaultTimeoutNs = 10ll * 1000 * 1000 * 1000;
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -131,13 +137,23 @@ uint32_t* default_err_buffer() {
 
 }  // namespace
 
+// Split group (tpf_comm_create_split_group): the per-rank launch parameters of one collective
+// call, collected from every rank's call; the last rank's call launches them all as one grid.
+struct SplitGroup {
+  int world = 0;
+  std::mutex mu;
+  tpf::GroupParams gp;
+  bool have[tpf::kMaxRanks] = {};
+  int npending = 0;
+  cudaStream_t stream = nullptr;
+};
+
 struct tpf_comm {
   int rank = 0;
   int world = 1;
   int local_group = 0;          // 1: all ranks hosted by this process (single GPU)
   size_t sym_bytes = 0;         // per rank
   char* local = nullptr;        // this process's allocation (all ranks if local_group)
-  char* virtual_peers = nullptr;  // tpf_comm_create_virtual: the heap every virtual peer aliases
   char* sym[tpf::kMaxRanks] = {};
   bool opened[tpf::kMaxRanks] = {};
   bool peers_ready = false;
@@ -152,8 +168,14 @@ struct tpf_comm {
   int compute_only = 0;
   char* scratch = nullptr;
   size_t scratch_bytes = 0;
+  // Scratch buffers outgrown by a later call. A CUDA graph that captured an earlier call keeps
+  // that call's scratch pointer, so an outgrown buffer is never freed before tpf_comm_destroy.
+  std::vector<char*> retired;
   unsigned long long* trace = nullptr;
   int64_t trace_cap = 0;
+  int is_virtual = 0;            // tpf_comm_create_virtual (peers alias the own heap: no blame)
+  int failing_rank = -1;         // resolved by the last tpf_comm_sync that reported TPF_E_PEER
+  std::shared_ptr<SplitGroup> group;  // tpf_comm_create_split_group: shared deferred launch
 };
 
 namespace {
@@ -213,6 +235,47 @@ struct Call {
   void* out;
   const int32_t* sched;  // T*T*3 or null (T == 1)
 };
+
+// Split group: record rank c->rank's launch parameters; the call of the group's last rank
+// launches every rank's parameters as one grid (n * ctas_per_rank CTAs, all resident).
+tpf::Status group_submit(tpf_comm* c, const tpf::KParams& p, cudaStream_t stream) {
+  SplitGroup& G = *c->group;
+  std::lock_guard<std::mutex> lock(G.mu);
+  auto reset = [&G] {
+    for (int r = 0; r < tpf::kMaxRanks; ++r) G.have[r] = false;
+    G.npending = 0;
+  };
+  if (G.have[c->rank]) {
+    reset();
+    return tpf::Status::invalid("split group: rank " + std::to_string(c->rank) +
+                                " made a second call before every rank made the first (calls are collective)");
+  }
+  if (G.npending > 0) {
+    int first = 0;
+    while (!G.have[first]) ++first;
+    const tpf::KParams& f = G.gp.p[first];
+    if (f.op != p.op || f.mode != p.mode || f.T != p.T || f.m != p.m || f.nmb != p.nmb || f.nnt != p.nnt ||
+        f.nkb != p.nkb || f.direct != p.direct || f.wire_f32 != p.wire_f32 || f.ctas_per_rank != p.ctas_per_rank) {
+      reset();
+      return tpf::Status::invalid("split group: rank " + std::to_string(c->rank) +
+                                  " made a different collective call than rank " + std::to_string(first));
+    }
+    if (stream != G.stream) {
+      reset();
+      return tpf::Status::invalid("split group: every rank must issue the call on the same stream");
+    }
+  }
+  G.gp.p[c->rank] = p;
+  G.have[c->rank] = true;
+  G.stream = stream;
+  if (++G.npending < G.world) return tpf::Status::ok();
+  G.gp.n = G.world;
+  reset();
+  cudaError_t e = tpf::launch_fused_group(G.gp, p.ctas_per_rank * G.world, stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return tpf::Status::cuda(std::string("split-group launch: ") + cudaGetErrorString(e));
+  return tpf::Status::ok();
+}
 
 tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   tpf::KParams p;
@@ -345,7 +408,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
       return tpf::Status::capacity("symmetric heap too small: call needs " +
                                    std::to_string(2 * (nslots * slot_bytes) + 2 * kFlagBytesPerParity) +
                                    " bytes per rank, communicator has " + std::to_string(c->sym_bytes));
-    if (nslots * flags_per_slot * 4 > kFlagBytesPerParity)
+    if (nslots * flags_per_slot * 4 > kFlagCapBytes)
       return tpf::Status::capacity("too many flags for one call");
     for (int r = 0; r < k.T; ++r) p.sym[r] = c->sym[r];
     p.flag_off[0] = 0;
@@ -368,6 +431,10 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
                                   CU_TENSOR_MAP_SWIZZLE_NONE);
         if (!s.good()) return s;
       }
+    }
+    if (!c->is_virtual) {
+      p.blame.T = k.T;
+      for (int x = 0; x < k.T; ++x) p.blame.table[x] = reinterpret_cast<uint32_t*>(c->sym[x] + kBlameOff);
     }
     // epoch: in device memory, advanced by the launch that opens the call
     p.epoch_dev = c->dev_epoch;
@@ -393,13 +460,16 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   int pairs = tpf::max_pairs();
   if (pairs <= 0) return tpf::Status::cuda("kernel cannot be resident (cluster occupancy 0)");
   pairs = std::min(pairs, sms / 2);
-  int pairs_per_rank = pairs / R;
+  // a split group's ranks share this GPU's SMs like a local group's hosted ranks
+  const int share = (c && c->group) ? c->world : R;
+  int pairs_per_rank = pairs / share;
   if (k.max_pairs_per_rank > 0) pairs_per_rank = std::min(pairs_per_rank, k.max_pairs_per_rank);
   if (pairs_per_rank < 1)
-    return tpf::Status::invalid("local group of " + std::to_string(R) + " ranks needs " +
-                                std::to_string(R) + " resident CTA pairs, device has " +
+    return tpf::Status::invalid("local group of " + std::to_string(share) + " ranks needs " +
+                                std::to_string(share) + " resident CTA pairs, device has " +
                                 std::to_string(pairs));
   p.ctas_per_rank = 2 * pairs_per_rank;
+  if (c && c->group && k.T > 1) return group_submit(c, p, stream);
   cudaError_t e = tpf::launch_fused(p, p.ctas_per_rank * R, stream);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) return tpf::Status::cuda(std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -407,6 +477,23 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
 }
 
 int hosted(const tpf_comm* c) { return c->local_group ? c->world : 1; }
+
+// Blame tables of every rank of c's group (disabled for T == 1 and the virtual group).
+tpf::Blame blame_of(const tpf_comm* c) {
+  tpf::Blame b;
+  std::memset(&b, 0, sizeof(b));
+  if (!c || c->world <= 1 || c->is_virtual) return b;
+  b.T = c->world;
+  for (int x = 0; x < c->world; ++x) b.table[x] = reinterpret_cast<uint32_t*>(c->sym[x] + kBlameOff);
+  return b;
+}
+
+// The attention paths are multi-launch sequences; a split group defers single launches only.
+tpf::Status check_not_split(const tpf_comm* c, const char* what) {
+  if (c && c->group && c->world > 1)
+    return tpf::Status::invalid(std::string(what) + " is not available on a split group (fused GEMM ops only)");
+  return tpf::Status::ok();
+}
 
 tpf::Status check_ready(const tpf_comm* c) {
   if (!c) return tpf::Status::invalid("null communicator");
@@ -416,6 +503,43 @@ tpf::Status check_ready(const tpf_comm* c) {
                                 " but the current device is " + std::to_string(dev));
   if (c->world > 1 && !c->peers_ready)
     return tpf::Status::invalid("communicator peers not opened (call tpf_comm_open_peers)");
+  return tpf::Status::ok();
+}
+
+// Device resources of a communicator: the symmetric heap (heap_bytes, zeroed), the error
+// record, the device epoch, the query-split counters, the side stream and its fork / join
+// events. On failure the caller releases what was allocated with tpf_comm_destroy.
+cudaError_t alloc_comm_resources(tpf_comm* c, size_t heap_bytes) {
+  cudaGetDevice(&c->device);
+  cudaError_t e = cudaMalloc(&c->local, heap_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->local, 0, heap_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&c->qs_ready, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e;
+}
+
+// Make c->scratch at least `bytes`. An outgrown buffer is retired, not freed: a CUDA graph that
+// captured an earlier call still addresses it, and replays may interleave with eager calls of
+// other shapes. Growing inside a stream capture is refused (cudaMalloc is not a
+// capturable operation): make one eager call of the largest shape before capturing.
+tpf::Status grow_scratch(tpf_comm* c, size_t bytes, cudaStream_t stream) {
+  if (c->scratch_bytes >= bytes) return tpf::Status::ok();
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone)
+    return tpf::Status::invalid("attention scratch must grow to " + std::to_string(bytes) +
+                                " bytes inside a CUDA graph capture; make one eager call of this shape first");
+  char* p = nullptr;
+  TPF_CUDA_TRY_STATUS(cudaMalloc(&p, bytes));
+  if (c->scratch) c->retired.push_back(c->scratch);
+  c->scratch = p;
+  c->scratch_bytes = bytes;
   return tpf::Status::ok();
 }
 
@@ -469,23 +593,9 @@ int tpf_comm_create(int rank, int world, size_t sym_bytes, tpf_comm** out) {
   c->world = world;
   c->sym_bytes = sym_bytes;
   c->timeout_ns = env_timeout_ns();
-  cudaGetDevice(&c->device);
-  cudaError_t e = cudaMalloc(&c->local, sym_bytes);
-  if (e == cudaSuccess) e = cudaMemset(c->local, 0, sym_bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->qs_ready, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  const cudaError_t e = alloc_comm_resources(c, sym_bytes);
   if (e != cudaSuccess) {
-    if (c->local) cudaFree(c->local);
-    if (c->err) cudaFree(c->err);
-    if (c->dev_epoch) cudaFree(c->dev_epoch);
-    delete c;
+    tpf_comm_destroy(c);  // releases whatever was allocated so far
     return fail(tpf::Status::cuda(std::string("tpf_comm_create: ") + cudaGetErrorString(e)));
   }
   c->sym[rank] = c->local;
@@ -531,23 +641,9 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
   c->local_group = 1;
   c->sym_bytes = per;
   c->timeout_ns = env_timeout_ns();
-  cudaGetDevice(&c->device);
-  cudaError_t e = cudaMalloc(&c->local, per * world);
-  if (e == cudaSuccess) e = cudaMemset(c->local, 0, per * world);
-  if (e == cudaSuccess) e = cudaMalloc(&c->err, tpf::kErrWords * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->err, 0, tpf::kErrWords * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->dev_epoch, 2 * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMemset(c->dev_epoch, 0, 2 * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&c->qs_ready, tpf::kMaxRanks * tpf::kMaxRanks * sizeof(uint32_t));
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  const cudaError_t e = alloc_comm_resources(c, per * world);
   if (e != cudaSuccess) {
-    if (c->local) cudaFree(c->local);
-    if (c->err) cudaFree(c->err);
-    if (c->dev_epoch) cudaFree(c->dev_epoch);
-    delete c;
+    tpf_comm_destroy(c);  // releases whatever was allocated so far
     return fail(tpf::Status::cuda(std::string("tpf_comm_create_local_group: ") + cudaGetErrorString(e)));
   }
   for (int r = 0; r < world; ++r) c->sym[r] = c->local + per * r;
@@ -568,8 +664,8 @@ int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
   tpf_comm* c = nullptr;
   int rc = tpf_comm_create(0, world, sym_bytes, &c);
   if (rc != TPF_OK) return rc;
-  cudaError_t e = cudaMalloc(&c->virtual_peers, c->sym_bytes);
-  if (e == cudaSuccess) e = cudaMemset(c->local, 0xFF, 2 * kFlagBytesPerParity);
+  c->is_virtual = 1;
+  cudaError_t e = cudaMemset(c->local, 0xFF, kBlameOff);  // every flag pre-set; blame table stays zero
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     tpf_comm_destroy(c);
@@ -581,13 +677,37 @@ int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
   return TPF_OK;
 }
 
+int tpf_comm_create_split_group(int world, size_t sym_bytes, tpf_comm** comms) {
+  if (!comms) return fail(tpf::Status::invalid("null output pointer"));
+  if (world < 1 || world > tpf::kMaxRanks)
+    return fail(tpf::Status::invalid("tpf_comm_create_split_group: world out of range (1..8)"));
+  auto group = std::make_shared<SplitGroup>();
+  group->world = world;
+  for (int r = 0; r < world; ++r) {
+    comms[r] = nullptr;
+    const int rc = tpf_comm_create(r, world, sym_bytes, &comms[r]);
+    if (rc != TPF_OK) {
+      const std::string msg = g_last_error;
+      for (int q = 0; q < r; ++q) tpf_comm_destroy(comms[q]);
+      g_last_error = msg;
+      return rc;
+    }
+    comms[r]->group = group;
+  }
+  // peers: the other communicators' heaps, as tpf_comm_open_peers maps them over CUDA IPC
+  for (int r = 0; r < world; ++r) {
+    for (int x = 0; x < world; ++x) comms[r]->sym[x] = comms[x]->local;
+    comms[r]->peers_ready = true;
+  }
+  return TPF_OK;
+}
+
 int tpf_comm_destroy(tpf_comm* c) {
   if (!c) return TPF_OK;
   cudaDeviceSynchronize();
   for (int r = 0; r < c->world; ++r)
     if (c->opened[r]) cudaIpcCloseMemHandle(c->sym[r]);
   if (c->local) cudaFree(c->local);
-  if (c->virtual_peers) cudaFree(c->virtual_peers);
   if (c->err) cudaFree(c->err);
   if (c->dev_epoch) cudaFree(c->dev_epoch);
   if (c->qs_ready) cudaFree(c->qs_ready);
@@ -595,11 +715,13 @@ int tpf_comm_destroy(tpf_comm* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->scratch) cudaFree(c->scratch);
+  for (char* r : c->retired) cudaFree(r);
   delete c;
   return TPF_OK;
 }
 
 int tpf_comm_rank(const tpf_comm* c) { return c ? c->rank : -1; }
+int tpf_comm_failing_rank(const tpf_comm* c) { return c ? c->failing_rank : -1; }
 int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
 
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
@@ -630,16 +752,46 @@ int tpf_comm_inject_fault(tpf_comm* c, int rank) {
 
 int tpf_comm_sync(tpf_comm* c, void* stream) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
+  if (c->group) {
+    std::lock_guard<std::mutex> lock(c->group->mu);
+    if (c->group->npending > 0)
+      return fail(tpf::Status::invalid("split group: a collective call is still waiting for " +
+                                       std::to_string(c->world - c->group->npending) + " rank(s) to make it"));
+  }
   TPF_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   uint32_t rec[tpf::kErrWords];
   TPF_CUDA_TRY(cudaMemcpy(rec, c->err, sizeof(rec), cudaMemcpyDeviceToHost));
   if (rec[0] != 0) {
     TPF_CUDA_TRY(cudaMemset(c->err, 0, sizeof(rec)));
-    const int rank = static_cast<int>(rec[1]);
+    const int waiter = static_cast<int>(rec[1]);
+    // Follow the blame chain (tpf::Blame) from the rank that timed out to the rank that failed:
+    // waiter -> the rank it waited on -> ... until a rank that was not blocked (it failed
+    // without recording, e.g. a dead process) or that named itself. Peers in other processes
+    // record their give-ups within microseconds of ours; a short grace covers the race.
+    int culprit = waiter;
+    uint32_t tab[tpf::kMaxRanks] = {};
+    const bool have_tables = c->world > 1 && !c->is_virtual && waiter >= 0 && waiter < c->world;
+    if (have_tables) {
+      std::this_thread::sleep_for(std::chrono::milliseconds(20));
+      char* own = c->local_group ? c->local : c->sym[c->rank];
+      TPF_CUDA_TRY(cudaMemcpy(tab, own + kBlameOff, sizeof(tab), cudaMemcpyDeviceToHost));
+      int r = waiter;
+      for (int n = 0; n <= c->world && tab[r] != 0; ++n) {
+        const int a = static_cast<int>(tab[r]) - 1;
+        if (a == r || a < 0 || a >= c->world) break;
+        r = a;
+      }
+      culprit = r;
+      const int nheaps = c->local_group ? c->world : 1;
+      for (int h = 0; h < nheaps; ++h)
+        TPF_CUDA_TRY(cudaMemset((c->local_group ? c->sym[h] : own) + kBlameOff, 0, tpf::kBlameBytes));
+    }
+    c->failing_rank = culprit;
     std::string what = rec[0] == 1 ? "peer flag wait timed out" : "pipeline barrier timed out";
-    return fail(tpf::Status::peer("rank " + std::to_string(rank) + " failed: " + what +
-                                  " (step " + std::to_string(static_cast<int>(rec[2])) +
-                                  ", tile " + std::to_string(static_cast<int>(rec[3])) + ")"));
+    return fail(tpf::Status::peer("rank " + std::to_string(culprit) + " failed: " + what + " (rank " +
+                                  std::to_string(waiter) + " gave up at step " +
+                                  std::to_string(static_cast<int>(rec[2])) + ", tile " +
+                                  std::to_string(static_cast<int>(rec[3])) + ")"));
   }
   return TPF_OK;
 }
@@ -758,7 +910,7 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* const qkv[3], const void
   const int64_t Dh = 128, G = batch * heads, sl = S / T, fw = static_cast<int64_t>(T) * heads * Dh;
   const int64_t recv_bytes = batch * sl * fw * 2;
   const int64_t nflags2 = G * (sl / 128) * 4;
-  if (nflags2 * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
+  if (nflags2 * T * 4 > kFlagCapBytes || recv_bytes > data_bytes_per_parity(c->sym_bytes))
     return tpf::Status::capacity("symmetric heap too small for the attention all-to-all");
   auto recv_at = [&](int rank, int par) {
     return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes);
@@ -803,10 +955,10 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* const qkv[3], const void
     uint32_t* f0 = flags_at(rank, 0);
     uint32_t* f1 = flags_at(rank, 1);
     tpf::launch_wait_flags2(f0, f1, static_cast<int64_t>(rank) * nflags2, c->dev_epoch, 0, c->timeout_ns, c->err,
-                            rank, stream);
+                            rank, blame_of(c), 0, nflags2, stream);
     const int64_t off = static_cast<int64_t>(rank + 1) * nflags2;
     tpf::launch_wait_flags2(f0 + off, f1 + off, static_cast<int64_t>(T - 1 - rank) * nflags2, c->dev_epoch, 0,
-                            c->timeout_ns, c->err, rank, stream);
+                            c->timeout_ns, c->err, rank, blame_of(c), off, nflags2, stream);
     tpf::launch_copy_by_parity(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank, 0), recv_at(rank, 1),
                                recv_bytes, c->dev_epoch, stream);
   }
@@ -818,6 +970,7 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
                       int64_t heads, int64_t S, int64_t Dh, int scale, void* stream_v) {
   // fuse_all_to_all_attention (Alg. 5, layers.cpp:174-218) on the GEMM kernel family.
   tpf::Status s = check_ready(c);
+  if (s.good()) s = check_not_split(c, "tpf_attention_a2a");
   if (!s.good()) return fail(s);
   const int T = c->world;
   if (batch < 1 || heads < 1 || S < 1 || Dh < 1)
@@ -833,7 +986,7 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   const Geometry gpv = geometry(G, sl, S, Dh);
   const int64_t nflags = static_cast<int64_t>(gpv.nmb) * gpv.nnt * 4;  // per source rank
   const int64_t recv_bytes = batch * sl * fw * 2;
-  if (nflags * T * 4 > kFlagBytesPerParity || recv_bytes > data_bytes_per_parity(c->sym_bytes))
+  if (nflags * T * 4 > kFlagCapBytes || recv_bytes > data_bytes_per_parity(c->sym_bytes))
     return fail(tpf::Status::capacity("symmetric heap too small for the attention all-to-all"));
   auto recv_at = [&](int rank, int par) {
     return c->sym[rank] + 2 * kFlagBytesPerParity + par * data_bytes_per_parity(c->sym_bytes);
@@ -855,13 +1008,8 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
     if (!cs.good()) return fail(cs);
   }
   const size_t sc_bytes = static_cast<size_t>(R) * G * sl * S * 4, pb_bytes = sc_bytes / 2;
-  if (c->scratch_bytes < sc_bytes + pb_bytes) {
-    if (c->scratch) cudaFree(c->scratch);
-    c->scratch = nullptr;
-    c->scratch_bytes = 0;
-    TPF_CUDA_TRY(cudaMalloc(&c->scratch, sc_bytes + pb_bytes));
-    c->scratch_bytes = sc_bytes + pb_bytes;
-  }
+  s = grow_scratch(c, sc_bytes + pb_bytes, stream);
+  if (!s.good()) return fail(s);
   float* scores = reinterpret_cast<float*>(c->scratch);
   char* probs = c->scratch + sc_bytes;
   // This multi-launch fallback computes parity-specific pointers on the host, so it opens
@@ -909,9 +1057,11 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   for (int h = 0; h < R; ++h) {
     const int rank = r0 + h;
     uint32_t* f = flags_of(rank);
-    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags, epoch, c->timeout_ns, c->err, rank, stream);
+    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags, epoch, c->timeout_ns, c->err, rank, blame_of(c), 0,
+                           nflags, stream);
     tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags, static_cast<int64_t>(T - 1 - rank) * nflags,
-                           epoch, c->timeout_ns, c->err, rank, stream);
+                           epoch, c->timeout_ns, c->err, rank, blame_of(c), static_cast<int64_t>(rank + 1) * nflags,
+                           nflags, stream);
     TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + h * recv_bytes, recv_of(rank), recv_bytes,
                                  cudaMemcpyDeviceToDevice, stream));
   }
@@ -926,6 +1076,7 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   // for every query slice (fused tcgen05 flash attention, local output), then the fused
   // GEMM-RS over the row-sharded output projection with the schedule's reduction order.
   tpf::Status s = check_ready(c);
+  if (s.good()) s = check_not_split(c, "tpf_query_split_attention");
   if (!s.good()) return fail(s);
   const int T = c->world;
   std::vector<int32_t> sched;
@@ -944,13 +1095,8 @@ int tpf_query_split_attention(tpf_comm* c, const void* q, const void* k, const v
   const int r0 = c->local_group ? 0 : c->rank;
   const int64_t G = batch * heads, hd = heads * Dh;
   const size_t ctx_bytes = static_cast<size_t>(R) * batch * S * hd * 2;
-  if (c->scratch_bytes < ctx_bytes) {
-    if (c->scratch) cudaFree(c->scratch);
-    c->scratch = nullptr;
-    c->scratch_bytes = 0;
-    TPF_CUDA_TRY(cudaMalloc(&c->scratch, ctx_bytes));
-    c->scratch_bytes = ctx_bytes;
-  }
+  s = grow_scratch(c, ctx_bytes, stream);
+  if (!s.good()) return fail(s);
   tpf::FmhaParams fp;
   std::memset(&fp, 0, sizeof(fp));
   const uint64_t dims[4] = {static_cast<uint64_t>(Dh), static_cast<uint64_t>(S), static_cast<uint64_t>(G),
@@ -1160,7 +1306,7 @@ static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, 
   up.B = batch; up.H = heads_total; up.hl = hl; up.S = S; up.sl = sl; up.Dh = Dh;
   up.T = T; up.R = R; up.rank0 = r0;
   up.ctas_per_rank = std::max(1, std::min(tpf::num_sms() / R, 132));
-  if ((flag_off + static_cast<int64_t>(T) * up.ctas_per_rank) * 4 > kFlagBytesPerParity)
+  if ((flag_off + static_cast<int64_t>(T) * up.ctas_per_rank) * 4 > kFlagCapBytes)
     return tpf::Status::capacity("flag block too small for the Ulysses all-to-all");
   for (int par = 0; par < 2; ++par)
     for (int x = 0; x < T; ++x) {
@@ -1174,7 +1320,7 @@ static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, 
   for (int hh = 0; hh < R; ++hh) {
     const int rank = r0 + hh;
     tpf::launch_wait_flags2(up.flags[0][rank], up.flags[1][rank], static_cast<int64_t>(T) * up.ctas_per_rank,
-                            c->dev_epoch, 0, c->timeout_ns, c->err, rank, stream);
+                            c->dev_epoch, 0, c->timeout_ns, c->err, rank, blame_of(c), 0, up.ctas_per_rank, stream);
   }
   inbox_local[0] = up.dst[0][r0];
   inbox_local[1] = up.dst[1][r0];
@@ -1198,6 +1344,7 @@ static tpf::Status check_ulysses(tpf_comm* c, int64_t batch, int64_t heads_total
 int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, void* q_out, void* k_out, void* v_out,
                     int64_t batch, int64_t heads_total, int64_t S, int64_t Dh, void* stream_v) {
   tpf::Status s = check_ready(c);
+  if (s.good()) s = check_not_split(c, "tpf_ulysses_a2a");
   if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
   if (!s.good()) return fail(s);
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
@@ -1217,6 +1364,7 @@ int tpf_ulysses_a2a(tpf_comm* c, const void* q, const void* k, const void* v, vo
 int tpf_ulysses_attention(tpf_comm* c, const void* q, const void* k, const void* v, void* out, int64_t batch,
                           int64_t heads_total, int64_t S, int64_t Dh, int scale, void* stream_v) {
   tpf::Status s = check_ready(c);
+  if (s.good()) s = check_not_split(c, "tpf_ulysses_attention");
   if (s.good()) s = check_ulysses(c, batch, heads_total, S, Dh);
   if (!s.good()) return fail(s);
   const int T = c->world;

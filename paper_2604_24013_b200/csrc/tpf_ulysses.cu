@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(kPushThreads) ulysses_push_kernel(UlyssesParam
     __threadfence_system();
     st_relaxed_sys(p.flags[par][threadIdx.x] + static_cast<int64_t>(rank) * p.ctas_per_rank + cta, epoch);
   }
-  if (threadIdx.x == 0) epoch_publish(p.epoch_dev, epoch);
+  if (threadIdx.x == 0) epoch_publish(p.epoch_dev, epoch, gridDim.x);
 }
 
 }  // namespace

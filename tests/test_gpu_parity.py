@@ -60,8 +60,24 @@ def _up8(v):
     return (v + 7) // 8 * 8
 
 
-def run_rs(T, kind, m, x_full, w_full, wire=tpf.F32, out_dtype=torch.float32, comm=None):
-    """Feature-shard x_full (B,S,K) and row-shard w_full (K,N) over T ranks; run GEMM-RS."""
+def _run_split(T, sym_bytes, call, comms=None):
+    """Per-rank calls on a split group (tpf_comm_create_split_group): rank r's communicator
+    gets rank r's own tensors, exactly as one process per GPU would; the last call launches."""
+    own = comms is None
+    if own:
+        comms = tpf.Communicator.split_group(T, sym_bytes)
+    for r in range(T):
+        call(comms[r], r)
+    for c in comms:
+        c.sync()
+    if own:
+        for c in comms:
+            c.close()
+
+
+def run_rs(T, kind, m, x_full, w_full, wire=tpf.F32, out_dtype=torch.float32, comm=None, split=False):
+    """Feature-shard x_full (B,S,K) and row-shard w_full (K,N) over T ranks; run GEMM-RS
+    (local group: one stacked call; split=True: T per-rank calls on a split group)."""
     B, S, K = x_full.shape
     N = w_full.shape[1]
     kl = K // T
@@ -70,6 +86,10 @@ def run_rs(T, kind, m, x_full, w_full, wire=tpf.F32, out_dtype=torch.float32, co
     w = torch.stack([bf16(_pad_last(w_full[r * kl:(r + 1) * kl].T, kp).T) for r in range(T)]).to(DEV)
     kl = kp
     out = torch.full((T, B, S // T, N), float("nan"), device=DEV, dtype=out_dtype)
+    if split:
+        _run_split(T, tpf.sym_bytes_rs(T, B, S, kl, N, m, wire),
+                   lambda c, r: c.gemm_rs(x[r], w[r], out[r], kind=kind, m=m, wire=wire), comm)
+        return out.to(torch.float64).cpu().numpy()
     own = comm is None
     if own:
         comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, B, S, kl, N, m, wire))
@@ -80,7 +100,7 @@ def run_rs(T, kind, m, x_full, w_full, wire=tpf.F32, out_dtype=torch.float32, co
     return out.to(torch.float64).cpu().numpy()
 
 
-def run_ag(T, m, x_full, w_full, act=tpf.ACT_NONE, out_dtype=torch.float32, comm=None):
+def run_ag(T, m, x_full, w_full, act=tpf.ACT_NONE, out_dtype=torch.float32, comm=None, split=False):
     """Sequence-slice x_full (B,S,K) and column-shard w_full (K,N); run AG-GEMM."""
     B, S, K = x_full.shape
     N = w_full.shape[1]
@@ -88,6 +108,10 @@ def run_ag(T, m, x_full, w_full, act=tpf.ACT_NONE, out_dtype=torch.float32, comm
     x = torch.stack([bf16(x_full[:, r * sl:(r + 1) * sl]) for r in range(T)]).to(DEV)
     w = torch.stack([bf16(w_full[:, r * nl:(r + 1) * nl]) for r in range(T)]).to(DEV)
     out = torch.full((T, B, S, nl), float("nan"), device=DEV, dtype=out_dtype)
+    if split:
+        _run_split(T, tpf.sym_bytes_ag(T, B, S, K, nl, m), lambda c, r: c.ag_gemm(x[r], w[r], out[r], m=m, act=act),
+                   comm)
+        return out.to(torch.float64).cpu().numpy()
     own = comm is None
     if own:
         comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ag(T, B, S, K, nl, m))
@@ -262,7 +286,7 @@ def test_argument_errors_match_reference():
     with pytest.raises(ValueError, match="granularity must be >= 1"):
         comm.gemm_rs(x, w, out, m=0)
     with pytest.raises(ValueError, match="not divisible"):
-        comm.gemm_rs(x[:, :, :62], w, out, m=1)
+        comm.gemm_rs(x[:, :, :62].contiguous(), w, out, m=1)
     with pytest.raises(ValueError, match="not divisible"):
         comm.ag_gemm(torch.zeros((T, 1, 3, 16), device=DEV, dtype=torch.bfloat16), w, out, m=2)
     with pytest.raises(tpf.ShapeError):
@@ -287,20 +311,25 @@ def test_capacity_error():
     comm.close()
 
 
-@pytest.mark.parametrize("op", ["rs", "ag"])
-def test_failed_rank_raises_group_error(op):
-    """A rank that stops publishing (fault injection) surfaces as GroupError, not a hang."""
+@pytest.mark.parametrize("op", ["rs_ring", "rs_pairwise", "rs_circular", "ag"])
+@pytest.mark.parametrize("bad", [0, 2, 3])
+def test_failed_rank_raises_group_error(op, bad):
+    """A rank that stops publishing (fault injection) surfaces as GroupError naming THAT rank
+    (GroupError::failing_rank, fabric.hpp:22-31; fabric_test.cpp:44-58), not one of the ranks
+    that timed out waiting on it, and not a hang."""
     T, B, S, K, N = 4, 1, 512, 256, 256
     comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, B, S, K, N, 1) + tpf.sym_bytes_ag(T, B, S, K, N, 1))
     comm.set_timeout_ms(200)
-    comm.inject_fault(2)
+    comm.inject_fault(bad)
     x = O.randint((B, S, K), 0, 5, 1)
     w = O.randint((K, N), -2, 2, 2)
-    with pytest.raises(tpf.GroupError, match="rank"):
-        if op == "rs":
-            run_rs(T, tpf.RING, 1, x, w, comm=comm)
-        else:
+    kind = {"rs_ring": tpf.RING, "rs_pairwise": tpf.PAIRWISE, "rs_circular": tpf.CIRCULAR}.get(op)
+    with pytest.raises(tpf.GroupError, match=f"^rank {bad} failed") as ei:
+        if op == "ag":
             run_ag(T, 1, x, w, comm=comm)
+        else:
+            run_rs(T, kind, 1, x, w, comm=comm)
+    assert ei.value.failing_rank() == bad
     comm.inject_fault(-1)
     # the communicator recovers for the next call
     assert np.array_equal(run_rs(T, tpf.RING, 1, x, w, comm=comm), O.row_parallel(T, tpf.RING, 1, x, w))
@@ -722,8 +751,9 @@ def test_failed_rank_raises_group_error_attention(op):
         comm.sync()
 
     comm.inject_fault(1)
-    with pytest.raises(tpf.GroupError, match="rank"):
+    with pytest.raises(tpf.GroupError, match="^rank 1 failed") as ei:
         call()
+    assert ei.value.failing_rank() == 1
     comm.inject_fault(-1)
     call()
     comm.close()
@@ -906,6 +936,47 @@ def test_cuda_graph_capture_attention_paths():
     with pytest.raises(ValueError, match="CUDA graph"):
         with torch.cuda.graph(graph2, stream=s):
             comm.attention_a2a(q32, q32, q32, o32, batch, 2, stream=s)
+    comm.close()
+
+
+def test_query_split_graph_survives_larger_eager_call():
+    """A graph that captured a query-split call keeps its context scratch: a later eager call of
+    a LARGER shape grows the scratch without freeing the captured buffer (it is retired until
+    the communicator is destroyed), so the next replay still reads and writes live memory and
+    reproduces its eager result. Growing the scratch inside a capture is refused loudly."""
+    T, batch, heads, Dh, D = 2, 1, 4, 128, 256
+    g = torch.Generator(device=DEV).manual_seed(12)
+
+    def inputs(S):
+        hs = [torch.randn((T, batch * heads // T, S, Dh), device=DEV, generator=g).to(torch.bfloat16)
+              for _ in range(3)]
+        w_o = (torch.randn((T, (heads // T) * Dh, D), device=DEV, generator=g) / 16).to(torch.bfloat16)
+        return hs, w_o, torch.empty((T, batch, S // T, D), device=DEV)
+
+    hs, w_o, o = inputs(512)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, batch, 2048, heads // T * Dh, D))
+    s = torch.cuda.Stream(DEV)
+    with torch.cuda.stream(s):
+        comm.query_split_attention(*hs, w_o, o, batch, heads // T, stream=s)
+    torch.cuda.synchronize()
+    want = o.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        comm.query_split_attention(*hs, w_o, o, batch, heads // T, stream=s)
+    hb, wb, ob = inputs(2048)  # 4x the context: the scratch must grow
+    with pytest.raises(ValueError, match="eager call"):
+        graph_b = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_b, stream=s):
+            comm.query_split_attention(*hb, wb, ob, batch, heads // T, stream=s)
+    with torch.cuda.stream(s):
+        comm.query_split_attention(*hb, wb, ob, batch, heads // T, stream=s)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        o.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        comm.sync(s)
+        assert torch.equal(o, want)
     comm.close()
 
 
