@@ -14,7 +14,17 @@ inside the timed region; `roofline` for the dominant kernel (the AG-GEMM launch)
 live with CUDA events on its stream; `cpu_baseline` = the reference's own CPU code
 (oracle/_ref, compiled from /root/reference) on a bounded sample, timed on this host.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+At N > 1 (one rank per GPU, NCCL for plumbing, CUDA-IPC symmetric heaps for the data) the
+line adds, per op, the plain per-rank GEMM of the same shapes (exposed comm = fused - plain,
+acceptance C6), the measured tail from a device trace (acceptance C4), and the NCCL
+all-gather / reduce-scatter + cuBLAS non-overlapped baseline run in the same job. At N = 1 it
+adds one GPU of a TP = 8 group at full scale (virtual peers) with the same comparisons.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--dry-run]
+
+`--gpus N` without a torchrun environment launches the N ranks itself (torch.distributed.run,
+127.0.0.1); under torchrun WORLD_SIZE must equal N. `--dry-run` exercises only the launcher
+and rank plumbing (gloo, no GPU).
 """
 import argparse
 import json
@@ -164,6 +174,40 @@ def run_reference_arm(args, rank, world):
 
 
 # ------------------------------------------------------------------ our arm
+def _events(n, k=3):
+    import torch
+    return [[torch.cuda.Event(enable_timing=True) for _ in range(k)] for _ in range(n)]
+
+
+def _timed_calls(fn, stream, n):
+    """n back-to-back calls between two events on the launch stream: device ms per call."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(n):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / n
+
+
+def traced_tail(comm, fn, dev):
+    """Measured no_tail_check (costmodel.cpp:163-176 on a %globaltimer timeline):
+    one traced call; per rank, the last peer-flag publication minus the end of the last GEMM
+    tile. Returns (max tail us over this process's ranks, steps seen)."""
+    import torch
+
+    from paper_2604_24013_b200 import trace
+    buf = trace.alloc(300000, dev)
+    torch.cuda.synchronize(dev)
+    comm.set_trace(buf)
+    fn()
+    comm.sync()
+    comm.set_trace(None)
+    summ = trace.summarize(trace.decode(buf))
+    return max((v["tail_us"] for v in summ.values()), default=0.0)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -219,7 +263,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(max(3, args.warmup)):  # keep the GPU busy while sampling settles
             ag(); rs()
     n = args.steps
-    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
+    ev = _events(n)
     barrier()
     torch.cuda.synchronize(dev)
     if sampler:
@@ -242,31 +286,30 @@ def run_ours(args, rank, world, local_rank):
     ag_ms, rs_ms = max_over_ranks(ag_ms), max_over_ranks(rs_ms)
     clocks = sampler.stop() if sampler else None
     flops_step = block_flops(SEQ)  # whole job
-
-    # ---- exposed communication: same kernels with flag waits / wire traffic disabled
-    exposed = {"ag_us": 0.0, "rs_us": 0.0, "block_us": 0.0} if T == 1 else None
-    if T > 1:
-        comm.set_compute_only(True)
-        for _ in range(2):
-            ag(); rs()
-        torch.cuda.synchronize(dev)
-        barrier()
-        evc = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(n)]
-        for i in range(n):
-            evc[i][0].record(stream)
-            ag()
-            evc[i][1].record(stream)
-            rs()
-            evc[i][2].record(stream)
-        torch.cuda.synchronize(dev)
-        comm.set_compute_only(False)
-        barrier()
-        c_ag = max_over_ranks(sum(e[0].elapsed_time(e[1]) for e in evc) / n)
-        c_rs = max_over_ranks(sum(e[1].elapsed_time(e[2]) for e in evc) / n)
-        exposed = {"ag_us": 1e3 * (ag_ms - c_ag), "rs_us": 1e3 * (rs_ms - c_rs),
-                   "block_us": 1e3 * (ag_ms + rs_ms - c_ag - c_rs),
-                   "compute_only_ag_ms": c_ag, "compute_only_rs_ms": c_rs}
     value = flops_step / (ms_step * 1e-3) / 1e12
+
+    # ---- exposed communication (acceptance C6, acceptance_test.cpp:334-366; paper overhead =
+    # e2e - compute): the fused op against the PLAIN per-rank GEMM of the same
+    # shapes (T = 1 tcgen05 kernel, no collective, same fused SwiGLU epilogue), max over ranks.
+    # At N = 1 the ops ARE the plain GEMMs.
+    if T > 1:
+        one = tpf.Communicator.create(0, 1, 0)
+        xg = torch.randn((1, SEQ, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
+        yg = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
+        p_ag = lambda: one.ag_gemm(xg, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)  # noqa: E731
+        p_rs = lambda: one.gemm_rs(act, w_dn, yg, stream=stream)  # noqa: E731
+        for _ in range(2):
+            p_ag(); p_rs()
+        plain_ag = max_over_ranks(_timed_calls(p_ag, stream, n))
+        plain_rs = max_over_ranks(_timed_calls(p_rs, stream, n))
+        one.close()
+        tail_ag = max_over_ranks(traced_tail(comm, ag, dev))
+        tail_rs = max_over_ranks(traced_tail(comm, rs, dev))
+    else:
+        plain_ag, plain_rs, tail_ag, tail_rs = ag_ms, rs_ms, 0.0, 0.0
+    exposed = {"ag_us": 1e3 * (ag_ms - plain_ag), "rs_us": 1e3 * (rs_ms - plain_rs),
+               "block_us": 1e3 * (ag_ms + rs_ms - plain_ag - plain_rs),
+               "definition": "t(fused op) - t(plain per-rank GEMM of the same shapes), device events, max over ranks"}
 
     # ---- e2e through the public API with pinned host buffers (copies timed).
     # Every step copies its input from pinned host memory and its result back; the copies
@@ -285,10 +328,6 @@ def run_ours(args, rank, world, local_rank):
     ev_done = [torch.cuda.Event() for _ in range(n)]
     ev_out = [torch.cuda.Event() for _ in range(n)]
 
-    def block(xin, yout):
-        ag(xin)
-        rs(yout)
-
     barrier()
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -305,7 +344,8 @@ def run_ours(args, rank, world, local_rank):
         stream.wait_event(ev_in[i])
         if i >= nbuf:
             stream.wait_event(ev_out[i - nbuf])  # y_dev[b] drained by step i-nbuf's D2H
-        block(x_dev[b], y_dev[b])
+        ag(x_dev[b])
+        rs(y_dev[b])
         ev_done[i].record(stream)
         with torch.cuda.stream(s_out):
             s_out.wait_event(ev_done[i])
@@ -320,36 +360,49 @@ def run_ours(args, rank, world, local_rank):
     h2d = x_host[0].numel() * x_host[0].element_size() * world
     d2h = y_host[0].numel() * y_host[0].element_size() * world
 
-    # ---- non-overlapped baseline: cuBLAS (+ NCCL all-gather / reduce-scatter for T > 1)
-    base_ms = None
+    # ---- non-overlapped baseline in the same run: cuBLAS (+ NCCL all-gather / reduce-scatter
+    # for T > 1), the reference's "baseline" strategy (experiment.cpp:789-836, fabric.cpp:132-181)
+    base = None
     try:
         xg = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
         yfull = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
+        bev = []
 
-        def base_step():
+        def base_step(rec=False):
+            e = _events(1, 4)[0] if rec else None
+            if e:
+                e[0].record(stream)
             if T > 1:
                 dist.all_gather_into_tensor(xg, x)
             else:
                 xg.copy_(x)
+            if e:
+                e[1].record(stream)
             gt = torch.matmul(xg.view(SEQ, D_MODEL), w_gate)
             up = torch.matmul(xg.view(SEQ, D_MODEL), w_up)
             a = torch.nn.functional.silu(gt) * up
             torch.matmul(a, w_dn, out=yfull.view(SEQ, D_MODEL))
+            if e:
+                e[2].record(stream)
             if T > 1:
                 dist.reduce_scatter_tensor(y, yfull)
+            if e:
+                e[3].record(stream)
+                bev.append(e)
         for _ in range(max(2, args.warmup)):
             base_step()
         torch.cuda.synchronize(dev)
         barrier()
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record(stream)
         for _ in range(n):
-            base_step()
-        b1.record(stream)
+            base_step(True)
         torch.cuda.synchronize(dev)
-        base_ms = max_over_ranks(b0.elapsed_time(b1) / n)
+        base_ms = max_over_ranks(bev[0][0].elapsed_time(bev[-1][3]) / n)
+        comm_ms = max_over_ranks(sum(e[0].elapsed_time(e[1]) + e[2].elapsed_time(e[3]) for e in bev) / n)
+        base = {"ms_per_step": base_ms, "tflops": flops_step / (base_ms * 1e-3) / 1e12,
+                "collectives_ms": comm_ms if T > 1 else 0.0, "speedup_ours": base_ms / ms_step,
+                "what": ("NCCL all_gather_into_tensor + cuBLAS gate/up + SwiGLU + cuBLAS down + NCCL "
+                         "reduce_scatter_tensor, non-overlapped" if T > 1 else "cuBLAS gate/up + SwiGLU + cuBLAS down")}
     except Exception as exc:  # baseline is informative only
-        base_ms = None
         print(f"[bench] baseline failed: {exc}", file=sys.stderr)
 
     # ---- CPU reference sample (rank 0 at N = 1). It runs before the per-GPU blocks below, so
@@ -364,15 +417,12 @@ def run_ours(args, rank, world, local_rank):
                    "sample": f"{cb['tokens']} tokens of the block ({cb['ranks']} simulated TP ranks, "
                              f"one thread each), {cb['seconds']:.1f} s of reference CPU work, host nproc={nproc}"}
 
-    # ---- one GPU of a TP=8 group at full scale (virtual peers), then the single-GPU
-    # emulation of TP=8 (one persistent launch hosts all 8 ranks)
+    # ---- one GPU of a TP=8 group at full scale (virtual peers)
     virt = None
     if world == 1 and args.emulate_tp > 1:
         virt = virtual_block(args, dev, stream, args.emulate_tp)
-    emu = None
-    if world == 1 and args.emulate_tp > 1:
-        emu = emulated_block(args, dev, stream, args.emulate_tp)
 
+    comm.close()
     if rank != 0:
         return
     pk = peaks()
@@ -403,9 +453,13 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": 2 * n,
         "ops": {
             "ag_gemm_swiglu": {"ms": ag_ms, "tflops": 2.0 * SEQ * D_MODEL * 2 * FFN / (ag_ms * 1e-3) / 1e12,
+                               "plain_gemm_ms": plain_ag, "fused_over_plain": ag_ms / plain_ag,
+                               "tail_us": tail_ag,
                                "note": "AG-GEMM gate||up with SwiGLU fused in the epilogue"},
-            "gemm_rs": {"ms": rs_ms, "tflops": 2.0 * SEQ * FFN * D_MODEL / (rs_ms * 1e-3) / 1e12},
+            "gemm_rs": {"ms": rs_ms, "tflops": 2.0 * SEQ * FFN * D_MODEL / (rs_ms * 1e-3) / 1e12,
+                        "plain_gemm_ms": plain_rs, "fused_over_plain": rs_ms / plain_rs, "tail_us": tail_rs},
             "exposed_comm_us": exposed,
+            "no_tail": tail_ag == 0.0 and tail_rs == 0.0,
         },
         "roofline": {"kernel": "tpf_fused_kernel (AG-GEMM gate||up + fused SwiGLU)", "bound": "tensor",
                      "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
@@ -421,11 +475,8 @@ def run_ours(args, rank, world, local_rank):
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
-    if base_ms:
-        out["baseline_cublas_nccl"] = {"ms_per_step": base_ms, "tflops": flops_step / (base_ms * 1e-3) / 1e12,
-                                       "speedup_ours": base_ms / ms_step}
-    if emu:
-        out["emulated"] = emu
+    if base:
+        out["baseline_cublas_nccl"] = base
     if virt:
         out["virtual_per_gpu"] = virt
     print(json.dumps(out))
@@ -435,9 +486,9 @@ def virtual_block(args, dev, stream, T):
     """One GPU of a real TP=T group at full scale: rank 0 with virtual peers (a self-ring: the
     peers alias this rank's heap, so every send fills the slot this rank reads one step later
     and the ring's step-to-step dependencies are real, with zero link latency) runs the cfg2
-    block's per-rank AG-GEMM +
-    SwiGLU and GEMM-RS with the whole protocol. Against compute-only mode this is the
-    protocol's on-GPU cost per GPU; NVLink latency is the part it cannot show."""
+    block's per-rank AG-GEMM + SwiGLU and GEMM-RS with the whole protocol, against the plain
+    per-rank GEMMs of the same shapes (acceptance C6: fused / plain), and a traced call of each
+    for the measured tail. NVLink latency is the part it cannot show."""
     import statistics
 
     import torch
@@ -446,119 +497,91 @@ def virtual_block(args, dev, stream, T):
     S_l, F_l = SEQ // T, FFN // T
     g = torch.Generator(device=dev).manual_seed(11)
     x = torch.randn((1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
+    xg = torch.randn((1, SEQ, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
     w_gu = (torch.randn((D_MODEL, 2 * F_l), device=dev, generator=g) / 64).to(torch.bfloat16)
     w_dn = (torch.randn((F_l, D_MODEL), device=dev, generator=g) / 120).to(torch.bfloat16)
     act = torch.empty((1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
     y = torch.empty((1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
+    y32 = torch.empty((1, S_l, D_MODEL), device=dev, dtype=torch.float32)
+    yg = torch.empty((1, SEQ, D_MODEL), device=dev, dtype=torch.bfloat16)
     comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
-                                                 tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
-
-    def timed(fn, n=20):
-        # n back-to-back calls between two events: the host runs ahead, so the figure is
-        # device time per call (a single synchronised call would also time the launch and
-        # the clock ramp of an idle GPU)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        fn()
-        e0.record(stream)
-        for _ in range(n):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        return e0.elapsed_time(e1) / n
+                                                 tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.F32)))
+    one = tpf.Communicator.create(0, 1, 0)
 
     ag = lambda: comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)  # noqa: E731
     rs = lambda: comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)  # noqa: E731
+    rs32 = lambda: comm.gemm_rs(act, w_dn, y32, kind=tpf.RING, wire=tpf.F32, stream=stream)  # noqa: E731
+    p_ag = lambda: one.ag_gemm(xg, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)  # noqa: E731
+    p_rs = lambda: one.gemm_rs(act, w_dn, yg, stream=stream)  # noqa: E731
     for _ in range(3):
-        ag(); rs()
-    res = {"ag": [], "rs": [], "ag_co": [], "rs_co": []}
-    for _ in range(5):
-        res["ag"].append(timed(ag))
-        res["rs"].append(timed(rs))
-        comm.set_compute_only(True)
-        res["ag_co"].append(timed(ag))
-        res["rs_co"].append(timed(rs))
-        comm.set_compute_only(False)
+        ag(); rs(); rs32(); p_ag(); p_rs()
+    res = {"ag": [], "rs": [], "rs32": [], "p_ag": [], "p_rs": []}
+    fns = {"ag": ag, "rs": rs, "rs32": rs32, "p_ag": p_ag, "p_rs": p_rs}
+    for _ in range(5):  # rounds alternate fused and plain, so both see the same power state
+        for k, fn in fns.items():
+            res[k].append(_timed_calls(fn, stream, 20))
     comm.sync(stream)
+    tail_ag = traced_tail(comm, ag, dev)
+    tail_rs = traced_tail(comm, rs, dev)
     comm.close()
+    one.close()
     m = {k: statistics.median(v) for k, v in res.items()}
     fl_ag, fl_rs = 2.0 * SEQ * D_MODEL * 2 * F_l, 2.0 * SEQ * F_l * D_MODEL
     # SURVEY 8(d) roofline: max(FLOPs at the measured bf16 burst peak, NVLink bytes at 900 GB/s)
     pk = peaks()["bf16_tflops"] * 1e12
-    wire = (T - 1) / T * SEQ * 2
-    t_roof_ag = max(fl_ag / pk, wire * D_MODEL / 900e9) * 1e3
-    t_roof_rs = max(fl_rs / pk, wire * D_MODEL / 900e9) * 1e3
+    rows_moved = (T - 1) / T * SEQ
+    t_roof_ag = max(fl_ag / pk, rows_moved * D_MODEL * 2 / 900e9) * 1e3
+    t_roof_rs = max(fl_rs / pk, rows_moved * D_MODEL * 2 / 900e9) * 1e3
+    t_roof_rs32 = max(fl_rs / pk, rows_moved * D_MODEL * 4 / 900e9) * 1e3
     return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (self-ring: "
                              "peers alias the own heap, sends fill the slot read one step later, zero link "
-                             "latency); medians of 5 rounds of 20 "
-                             "back-to-back calls per op",
-            "ag_gemm_ms": m["ag"], "gemm_rs_ms": m["rs"], "compute_only_ag_ms": m["ag_co"],
-            "compute_only_rs_ms": m["rs_co"],
+                             "latency); medians of 5 rounds of 20 back-to-back calls per op; plain = the T = 1 "
+                             "kernel on the same per-rank shapes",
+            "ag_gemm_ms": m["ag"], "gemm_rs_ms": m["rs"], "gemm_rs_f32_wire_ms": m["rs32"],
+            "plain_ag_gemm_ms": m["p_ag"], "plain_gemm_rs_ms": m["p_rs"],
+            "fused_over_plain": {"ag": m["ag"] / m["p_ag"], "rs": m["rs"] / m["p_rs"]},
+            "exposed_comm_us": {"ag": 1e3 * (m["ag"] - m["p_ag"]), "rs": 1e3 * (m["rs"] - m["p_rs"])},
+            "tail_us": {"ag": tail_ag, "rs": tail_rs},
             "ag_tflops_per_gpu": fl_ag / (m["ag"] * 1e-3) / 1e12, "rs_tflops_per_gpu": fl_rs / (m["rs"] * 1e-3) / 1e12,
-            "protocol_overhead_us": {"ag": 1e3 * (m["ag"] - m["ag_co"]), "rs": 1e3 * (m["rs"] - m["rs_co"])},
-            "t_roof_ms": {"ag": t_roof_ag, "rs": t_roof_rs},
-            "frac_of_t_roof": {"ag": t_roof_ag / m["ag"], "rs": t_roof_rs / m["rs"]}}
+            "t_roof_ms": {"ag": t_roof_ag, "rs": t_roof_rs, "rs_f32_wire": t_roof_rs32},
+            "frac_of_t_roof": {"ag": t_roof_ag / m["ag"], "rs": t_roof_rs / m["rs"],
+                               "rs_f32_wire": t_roof_rs32 / m["rs32"]}}
 
 
-def emulated_block(args, dev, stream, T):
-    """cfg2 block at TP=T with all T ranks hosted on this GPU in one launch per op
-    (each rank on 148/T SMs; 'peer' buffers in local HBM). Same FLOPs as the T=1 run,
-    so the ratio exposes the fused protocol's overhead (flags, wire copies, forwarding)."""
+# ------------------------------------------------------------- launch / dry run
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` without a torchrun environment: launch N ranks (one per GPU) through
+    torch.distributed.run on 127.0.0.1 and return the group's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank harness without GPUs (gloo): rendezvous, barrier, max-over-ranks
+    reduction and the one JSON line from rank 0. Used by the CPU test of the launcher."""
     import torch
-
-    import paper_2604_24013_b200 as tpf
-    S_l, F_l = SEQ // T, FFN // T
-    g = torch.Generator(device=dev).manual_seed(7)
-    x = torch.randn((T, 1, S_l, D_MODEL), device=dev, generator=g).to(torch.bfloat16)
-    w_gu = (torch.randn((T, D_MODEL, 2 * F_l), device=dev, generator=g) / 64).to(torch.bfloat16)
-    w_dn = (torch.randn((T, F_l, D_MODEL), device=dev, generator=g) / 120).to(torch.bfloat16)
-    act = torch.empty((T, 1, SEQ, F_l), device=dev, dtype=torch.bfloat16)
-    y = torch.empty((T, 1, S_l, D_MODEL), device=dev, dtype=torch.bfloat16)
-    comm = tpf.Communicator.local_group(T, max(tpf.sym_bytes_ag(T, 1, SEQ, D_MODEL, 2 * F_l, 1),
-                                               tpf.sym_bytes_rs(T, 1, SEQ, F_l, D_MODEL, 1, tpf.BF16)))
-
-    def step():
-        comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
-        comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
-
-    import statistics
-
-    for _ in range(args.warmup):
-        step()
-    comm.sync(stream)
-
-    def timed(k):
-        # k back-to-back steps, per-op events on the launch stream
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(k)]
-        for i in range(k):
-            ev[i][0].record(stream)
-            comm.ag_gemm(x, w_gu, act, act=tpf.ACT_SWIGLU, stream=stream)
-            ev[i][1].record(stream)
-            comm.gemm_rs(act, w_dn, y, kind=tpf.RING, wire=tpf.BF16, stream=stream)
-            ev[i][2].record(stream)
-        torch.cuda.synchronize(dev)
-        return (ev[0][0].elapsed_time(ev[-1][2]) / k, sum(e[0].elapsed_time(e[1]) for e in ev) / k,
-                sum(e[1].elapsed_time(e[2]) for e in ev) / k)
-
-    # fused and compute-only rounds alternate (medians), so both see the same power state
-    k = max(3, min(args.steps, 10))
-    fused, conly = [], []
-    for _ in range(5):
-        comm.set_compute_only(False)
-        fused.append(timed(k))
-        comm.set_compute_only(True)
-        conly.append(timed(k))
-    comm.set_compute_only(False)
-    comm.sync(stream)
-    total, ag, rs = (statistics.median(c) for c in zip(*fused))
-    _, c_ag, c_rs = (statistics.median(c) for c in zip(*conly))
-    comm.close()
-    return {"tp": T, "note": "all ranks on ONE GPU (local group, each rank on 148/T SMs); wire traffic "
-                             "goes through local HBM, not NVLink; medians of 5 alternating fused / "
-                             "compute-only rounds",
-            "ms_per_step": total, "tflops": block_flops(SEQ) / (total * 1e-3) / 1e12,
-            "ag_gemm_ms": ag, "gemm_rs_ms": rs, "compute_only_ag_ms": c_ag, "compute_only_rs_ms": c_rs,
-            "exposed_comm_us": {"ag": 1e3 * (ag - c_ag), "rs": 1e3 * (rs - c_rs),
-                                "block": 1e3 * (ag + rs - c_ag - c_rs)}}
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "ranks_seen": int(t.item()),
+                          "steps": args.steps, "warmup": args.warmup, "impl": args.impl}))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -567,13 +590,22 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--emulate-tp", type=int, default=8, help="single-GPU local-group TP (N=1 only; 0 = off)")
+    ap.add_argument("--emulate-tp", type=int, default=8, help="per-GPU TP group model at N=1 (0 = off)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference sample")
+    ap.add_argument("--dry-run", action="store_true", help="launcher / rank plumbing only (gloo, no GPU)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU", file=sys.stderr)
+        sys.exit(2)
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
