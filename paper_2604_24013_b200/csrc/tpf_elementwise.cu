@@ -99,7 +99,8 @@ __device__ __forceinline__ void wait_flag_range(const uint32_t* flags, int64_t n
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     while (ld_relaxed_sys(flags + i) < epoch) {
-      const bool abort = ld_relaxed_sys(err + 4) != 0;
+      const bool abort = ld_relaxed_sys(err + 4) != 0 ||
+                         (blame.table[0] && ld_relaxed_sys(blame.table[rank] + kBlameAbort) == epoch);
       if (abort || globaltimer() - t0 > static_cast<uint64_t>(timeout_ns)) {
         if (!abort && atomicCAS(err, 0u, 1u) == 0u) {
           err[1] = static_cast<uint32_t>(rank);
@@ -107,6 +108,7 @@ __device__ __forceinline__ void wait_flag_range(const uint32_t* flags, int64_t n
           err[3] = static_cast<uint32_t>(i);
         }
         blame_store(blame.table, blame.T, rank, static_cast<int>((first + i) / per_src));
+        if (!abort) group_abort_store(blame.table, blame.T, kBlameAbort, epoch);
         atomicExch(err + 4, 1u);
         return;
       }

@@ -42,7 +42,12 @@ enum Mode : int {
 // that failed -- the reference's GroupError::failing_rank (fabric.hpp:22-31, 207-219), not a
 // victim. Entry [waiter] = awaited + 1; a rank that failed itself (fault injection) stores its
 // own rank + 1. The table sits at the end of the parity-1 flag block.
+// Word kBlameAbort of the table is the group abort flag: the first waiter to time out sets it in
+// every rank's table, and every rank's waiters give up at once (recording what they waited on)
+// -- the reference's "other ranks blocked on receives are woken and unwound" (fabric.hpp:185-189)
+// -- instead of each process draining garbage into its successors' waits.
 constexpr int64_t kBlameBytes = 256;
+constexpr int kBlameAbort = kMaxRanks;
 struct Blame {
   uint32_t* table[kMaxRanks];  // every rank's table (peer-mapped); table[0] null: disabled
   int T;

@@ -93,8 +93,11 @@ __device__ __forceinline__ void trace_rec(const KParams& p, int kind, int rank, 
   r[3] = t1;
 }
 
-__device__ __forceinline__ bool aborted(const KParams& p) {
-  return ld_relaxed_sys(p.err + 4) != 0;
+// This launch's error record says abort, or any rank of the group has set the group abort flag
+// in this rank's blame table (tpf::kBlameAbort).
+__device__ __forceinline__ bool aborted(const KParams& p, int rank, uint32_t epoch) {
+  if (ld_relaxed_sys(p.err + 4) != 0) return true;
+  return p.blame.table[0] != nullptr && ld_relaxed_sys(p.blame.table[rank] + kBlameAbort) == epoch;
 }
 
 __device__ __noinline__ void record_error(const KParams& p, uint32_t code, int rank, int step,
@@ -108,9 +111,11 @@ __device__ __noinline__ void record_error(const KParams& p, uint32_t code, int r
 }
 
 // A waiter gives up on rank `awaited`: blame entry for the failing-rank chain (tpf::Blame).
-__device__ __noinline__ void give_up(const KParams& p, bool timed_out, int rank, int awaited, int step, int tile) {
+__device__ __noinline__ void give_up(const KParams& p, bool timed_out, int rank, int awaited, int step, int tile,
+                                     uint32_t epoch) {
   if (timed_out) record_error(p, 1, rank, step, tile);
   blame_store(p.blame.table, p.blame.T, rank, awaited);
+  if (timed_out) group_abort_store(p.blame.table, p.blame.T, kBlameAbort, epoch);
 }
 
 // Bounded spin on a flag written by rank `awaited` (value >= epoch). Returns with acquire
@@ -133,8 +138,8 @@ __device__ __forceinline__ bool wait_flag(const KParams& p, const uint32_t* f, i
       __nanosleep(32);
     }
     const bool timed_out = globaltimer() - t0 > static_cast<uint64_t>(p.timeout_ns);
-    if (aborted(p) || timed_out) {
-      give_up(p, timed_out && !aborted(p), rank, awaited, step, tile);
+    if (aborted(p, rank, epoch) || timed_out) {
+      give_up(p, timed_out && !aborted(p, rank, epoch), rank, awaited, step, tile, epoch);
       return false;
     }
   }
@@ -496,7 +501,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
           if (ld_acquire_gpu(cnt) < p.qs_target) {
             const uint64_t tq0 = globaltimer();
             while (ld_acquire_gpu(cnt) < p.qs_target) {
-              if (aborted(p)) break;
+              if (aborted(p, rank, ep)) break;
               if (globaltimer() - tq0 > static_cast<uint64_t>(p.timeout_ns)) {
                 record_error(p, 1, rank, t.step, lin);
                 break;
@@ -528,8 +533,9 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
               __nanosleep(32);
               if ((poll & 255) == 255) {
                 const bool timed_out = globaltimer() - tspin > static_cast<uint64_t>(p.timeout_ns);
-                if (aborted(p) || timed_out) {
-                  if (lane == 0) give_up(p, timed_out && !aborted(p), rank, p.sched[rank][it - 1][1], t.step, lin);
+                if (aborted(p, rank, ep) || timed_out) {
+                  if (lane == 0)
+                    give_up(p, timed_out && !aborted(p, rank, ep), rank, p.sched[rank][it - 1][1], t.step, lin, ep);
                   break;
                 }
               }

@@ -253,6 +253,16 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+// Group abort (tpf::Blame): word `abort_word` of all T ranks' tables := the aborted call's epoch
+// (the ranks of a group advance their epochs in lockstep, so a stale abort of an earlier call
+// never matches a later one).
+__device__ __forceinline__ void group_abort_store(uint32_t* const* tables, int T, int abort_word, uint32_t epoch) {
+  if (!tables[0]) return;
+  for (int x = 0; x < T; ++x) st_relaxed_sys(tables[x] + abort_word, epoch);
+  fence_sys();
+}
+
+
 // Blame record (tpf::Blame): entry [waiter] = awaited + 1 in all T ranks' tables. Called by a
 // waiter that gives up on a peer flag; awaited == waiter marks a rank that failed itself.
 __device__ __forceinline__ void blame_store(uint32_t* const* tables, int T, int waiter, int awaited) {

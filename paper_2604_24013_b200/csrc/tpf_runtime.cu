@@ -761,6 +761,20 @@ int tpf_comm_sync(tpf_comm* c, void* stream) {
   TPF_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   uint32_t rec[tpf::kErrWords];
   TPF_CUDA_TRY(cudaMemcpy(rec, c->err, sizeof(rec), cudaMemcpyDeviceToHost));
+  if (rec[0] == 0 && c->world > 1 && !c->is_virtual) {
+    // A rank that did not fail this call may still hold blame entries or the group abort flag
+    // written by the others (or its own fault-injection mark): clear them for the next call.
+    char* own = c->local_group ? c->local : c->sym[c->rank];
+    uint32_t tab[tpf::kBlameBytes / 4];
+    TPF_CUDA_TRY(cudaMemcpy(tab, own + kBlameOff, sizeof(tab), cudaMemcpyDeviceToHost));
+    bool dirty = false;
+    for (uint32_t v : tab) dirty |= v != 0;
+    if (dirty) {
+      const int nheaps = c->local_group ? c->world : 1;
+      for (int h = 0; h < nheaps; ++h)
+        TPF_CUDA_TRY(cudaMemset((c->local_group ? c->sym[h] : own) + kBlameOff, 0, tpf::kBlameBytes));
+    }
+  }
   if (rec[0] != 0) {
     TPF_CUDA_TRY(cudaMemset(c->err, 0, sizeof(rec)));
     const int waiter = static_cast<int>(rec[1]);

@@ -58,7 +58,8 @@ def summarize(recs: list[Rec]) -> dict:
     out = {}
     for rank, kinds in sorted(per_rank.items()):
         tiles = kinds.get(TR_TILE, [])
-        comm = kinds.get(TR_FLAG, []) + kinds.get(TR_AG_PIECE, [])
+        # transfers: RS flags published (by the epilogue or the publisher warp), AG images forwarded
+        comm = kinds.get(TR_FLAG, []) + kinds.get(TR_PUBLISH, []) + kinds.get(TR_AG_PIECE, [])
         steps = defaultdict(lambda: [None, None])
         for r in kinds.get(TR_MAINLOOP, []):
             s = steps[r.step]

@@ -12,6 +12,7 @@ import paper_2604_24013_b200 as tpf
 from paper_2604_24013_b200 import trace
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+STEADY = "steady" in sys.argv[3:]
 cfg = sys.argv[2] if len(sys.argv) > 2 else "cfg2"
 S, K_ag, N_ag, K_rs, N_rs = {"cfg2": (8192, 4096, 28672, 14336, 4096),
                              "cfg3": (16384, 8192, 10240, 8192, 8192)}[cfg]
@@ -34,10 +35,16 @@ def show(name, fn, compute_only=False):
     torch.cuda.synchronize()
     buf = trace.alloc(400000)
     torch.cuda._sleep(2_000_000)  # keep the GPU busy while the host enqueues the traced call
+    if STEADY:  # the traced call runs between back-to-back calls, as in the timed loops
+        for _ in range(3):
+            fn()
     comm.set_trace(buf)
     fn()
-    comm.sync()
     comm.set_trace(None)
+    if STEADY:
+        for _ in range(3):
+            fn()
+    comm.sync()
     comm.set_compute_only(False)
     recs = trace.decode(buf)
     t0 = min(r.t0 for r in recs if r.t0 > 0)
@@ -66,6 +73,17 @@ def show(name, fn, compute_only=False):
     fin = sorted(((max(r.t1 for r in v) - t0) / 1e3, b) for b, v in by.items())
     print(f"    per-block main-loop busy: min {busy[0][0]:.1f} median {busy[len(busy) // 2][0]:.1f} max {busy[-1][0]:.1f} us;"
           f" slowest blocks {[b for _, b in busy[-6:]]}, last to finish {[b for _, b in fin[-6:]]}", flush=True)
+    # per step: first main-loop start, last main-loop end, last epilogue end (us from t0)
+    steps = {}
+    for r in ml:
+        st = steps.setdefault(r.step, [1e18, 0, 0])
+        st[0] = min(st[0], r.t0)
+        st[1] = max(st[1], r.t1)
+    for r in ep:
+        steps.setdefault(r.step, [1e18, 0, 0])[2] = max(steps[r.step][2], r.t1)
+    print("    steps (mainloop first start / last end / last epilogue end, us): " +
+          " ".join(f"{k}:{(v[0] - t0) / 1e3:.0f}/{(v[1] - t0) / 1e3:.0f}/{(v[2] - t0) / 1e3:.0f}"
+                   for k, v in sorted(steps.items())), flush=True)
     for kind in (trace.TR_EPI_LOOP, trace.TR_PUBLISH, trace.TR_FLUSH, trace.TR_WAIT_IN, trace.TR_WAIT_A):
         rr = [r for r in recs if r.kind == kind]
         if rr:
