@@ -53,19 +53,30 @@ struct Tile {
 };
 
 // Pair-tile raster: step-major; inside a step, group_m m-block pairs sweep the n-tiles.
+// With group_n > 0 the roles swap: group_n n-tiles are swept by all m-block pairs (keeps a
+// slab of B L2-resident while A streams; narrow-N, long-K shapes).
 __device__ __forceinline__ Tile get_tile(const KParams& p, int lin, int cta) {
-  const int GM = p.group_m;
   const int per_step = p.npairs * p.nnt;
   Tile t;
   t.step = lin / per_step;
   const int rem = lin - t.step * per_step;
-  const int g0 = (rem / (GM * p.nnt)) * GM;
-  const int gm = min(GM, p.npairs - g0);
-  const int r2 = rem - g0 * p.nnt;
-  // Pairs never straddle a batch: the pair shares one B tile (cta_group::2), and with a
-  // per-batch B (attention heads) both CTAs must be in the same batch.
-  t.pair = g0 + r2 % gm;
-  t.nt = r2 / gm;
+  if (p.group_n > 0) {
+    const int GN = p.group_n;
+    const int g0 = (rem / (GN * p.npairs)) * GN;
+    const int gn = min(GN, p.nnt - g0);
+    const int r2 = rem - g0 * p.npairs;
+    t.nt = g0 + r2 % gn;
+    t.pair = r2 / gn;
+  } else {
+    const int GM = p.group_m;
+    const int g0 = (rem / (GM * p.nnt)) * GM;
+    const int gm = min(GM, p.npairs - g0);
+    const int r2 = rem - g0 * p.nnt;
+    // Pairs never straddle a batch: the pair shares one B tile (cta_group::2), and with a
+    // per-batch B (attention heads) both CTAs must be in the same batch.
+    t.pair = g0 + r2 % gm;
+    t.nt = r2 / gm;
+  }
   const int ppb = (p.nmb_per_batch + 1) / 2;
   t.b = t.pair / ppb;
   const int j = 2 * (t.pair - t.b * ppb) + cta;
@@ -362,7 +373,9 @@ __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t
 // T = 1 MLP block; on the per-GPU TP = 8 fused GEMM-RS PDL cost 5% with every trigger
 // placement (after the prologue, after the last TMA load, implicit at exit), and it was
 // neutral on the fused AG-GEMM, so the multi-rank instances keep plain stream order.
-__host__ __device__ constexpr bool pdl_instance(int mode) { return mode == MODE_SINGLE; }
+__host__ __device__ constexpr bool pdl_instance(int mode) {
+  return mode == MODE_SINGLE || mode == MODE_STD || mode == MODE_DP_GRAD || mode == MODE_GATHER_B;
+}
 
 // Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
 // single-thread producer / MMA loops cost measurable throughput.
@@ -465,6 +478,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       // With AG wire inputs the whole warp walks the schedule (the wire-image flag scan is
       // warp-parallel); otherwise lane 0 alone. Lane 0 issues barrier arrivals and TMA loads.
       const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
+      const uint64_t pol_a = l2_policy(p.l2_a), pol_b = l2_policy(p.l2_b);
       int stage = 0;
       uint32_t phase = 0;
       for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
@@ -570,7 +584,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
                 tma_load_2sm_4d(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
                                 t.b, h);
             } else {
-              tma_load_2sm_4d(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h);
+              tma_load_2sm_4d_hint(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h, pol_a);
             }
             if (b_from_wire) {
               tma_load_2sm_5d(sb, wmap, fb, 0, 0, img, aslot, h);
@@ -587,8 +601,8 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
                   tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                                   kb * BK, t.b, h);
                 else
-                  tma_load_2sm_3d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
-                                  kb * BK, h);
+                  tma_load_2sm_3d_hint(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                                       kb * BK, h, pol_b);
               }
             }
             if (p.trace && kb == 0) t_first = globaltimer();
@@ -1015,6 +1029,16 @@ int pdl_setting() {
   return v;
 }
 bool pdl_enabled() { return pdl_setting() != 0; }
+// TPF_PDL_FUSED=1 (A/B switch): the multi-rank GEMM instances launch with PDL too. Safe: a
+// dependent grid's CTAs pass griddepcontrol.wait only once this grid has completed, so none of
+// its cross-CTA waits can start before the whole grid is resident.
+bool pdl_fused_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("TPF_PDL_FUSED");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 
 template <int kOp, int kMode, typename Params>
 cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
@@ -1060,7 +1084,8 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
   } else {
-    cfg.numAttrs = (pdl_instance(kMode) && pdl_enabled()) ? 2 : 1;
+    const bool pdl = kMode == MODE_SINGLE ? pdl_enabled() : (pdl_instance(kMode) && pdl_fused_enabled());
+    cfg.numAttrs = pdl ? 2 : 1;
     KParams q = p;
     q.pdl_trigger = pdl_setting() == 3 ? 0 : pdl_setting();
     return cudaLaunchKernelEx(&cfg, kern, q);

@@ -368,7 +368,25 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.npairs = g.npairs;
   for (int h = 0; h < R; ++h) p.qs_ready[h] = k.qs_ready[h];
   p.qs_target = k.qs_target;
+  // Raster and L2 residency. Multi-rank instances: groups of 16 m-block pairs sweep the
+  // n-tiles. T == 1 GEMMs (measured on the bench block, tools/l2_probe.py, profiles/r02_l2_raster.txt):
+  // narrow N (fewer n-tiles than m-block pairs, e.g. the 8192x14336x4096 down projection):
+  // half the n-tiles are swept by every m-block pair with that B slab marked evict_last
+  // (-3.5% time, -22% DRAM bytes); otherwise the m-group's A panels are marked evict_last.
   p.group_m = env_group_m();
+  p.group_n = 0;
+  p.l2_a = p.l2_b = 0;
+  if (p.mode == tpf::MODE_SINGLE) {
+    if (g.nnt < g.npairs) {
+      p.group_n = std::max(1, g.nnt / 2);
+      p.l2_b = 2;
+    } else {
+      p.l2_a = 2;
+    }
+  }
+  if (const char* e = std::getenv("TPF_GROUP_N")) p.group_n = std::atoi(e);  // dev A/B overrides
+  if (const char* e = std::getenv("TPF_L2_A")) p.l2_a = std::atoi(e);
+  if (const char* e = std::getenv("TPF_L2_B")) p.l2_b = std::atoi(e);
   p.ag_nfwd = env_int("TPF_AG_NFWD", 4);
   p.ag_batch = env_int("TPF_AG_BATCH", 4);
   p.nsteps = k.T * k.m;
