@@ -672,11 +672,12 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
 
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
   // Performance-only: rank 0 of a `world`-rank group on this GPU, with every peer virtual.
-  // Peer heaps alias this rank's own heap, so a send lands in this rank's inbox slot of the
-  // same index -- the slot the real successor would fill -- and is read back one step later
-  // while still L2-resident, as data arriving over NVLink would be. This rank's flag blocks
-  // are pre-set to 0xFFFFFFFF (sends write the call's epoch, which still passes), so every
-  // peer wait passes at once and wire / inbox contents are stale.
+  // Peer heaps alias this rank's own heap (a self-ring), so a send lands in this rank's inbox
+  // slot of the same index -- the slot the real successor would fill -- and is read one step
+  // later while still L2-resident, as data arriving over NVLink would be. The flag blocks start
+  // pre-set to 0xFFFFFFFF only so that the FIRST call after creation does not wait on flags
+  // nobody writes; every send overwrites its flag with the call's epoch, so from the second
+  // call on each step's wait is real: it passes when this rank's own previous-step send lands.
   // The kernels run the real protocol instructions at full-GPU scale, which measures what one
   // GPU of a TP group computes. Results are NOT meaningful.
   tpf_comm* c = nullptr;

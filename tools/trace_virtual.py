@@ -75,6 +75,7 @@ def show(name, fn, compute_only=False):
           f" slowest blocks {[b for _, b in busy[-6:]]}, last to finish {[b for _, b in fin[-6:]]}", flush=True)
     # per step: first main-loop start, last main-loop end, last epilogue end (us from t0)
     steps = {}
+    tk = min(r.t0 for r in recs if r.t0 > 0)
     for r in ml:
         st = steps.setdefault(r.step, [1e18, 0, 0])
         st[0] = min(st[0], r.t0)
@@ -82,7 +83,7 @@ def show(name, fn, compute_only=False):
     for r in ep:
         steps.setdefault(r.step, [1e18, 0, 0])[2] = max(steps[r.step][2], r.t1)
     print("    steps (mainloop first start / last end / last epilogue end, us): " +
-          " ".join(f"{k}:{(v[0] - t0) / 1e3:.0f}/{(v[1] - t0) / 1e3:.0f}/{(v[2] - t0) / 1e3:.0f}"
+          " ".join(f"{k}:{(v[0] - tk) / 1e3:.0f}/{(v[1] - tk) / 1e3:.0f}/{(v[2] - tk) / 1e3:.0f}"
                    for k, v in sorted(steps.items())), flush=True)
     for kind in (trace.TR_EPI_LOOP, trace.TR_PUBLISH, trace.TR_FLUSH, trace.TR_WAIT_IN, trace.TR_WAIT_A):
         rr = [r for r in recs if r.kind == kind]
@@ -93,6 +94,8 @@ def show(name, fn, compute_only=False):
 
 show("AG", lambda: comm.ag_gemm(x, w, y))
 show("AG", lambda: comm.ag_gemm(x, w, y), True)
+if "pairwise" in sys.argv[3:]:
+    show("RS pairwise", lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.PAIRWISE, wire=tpf.BF16))
 show("RS", lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16))
 show("RS", lambda: comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16), True)
 comm.close()
