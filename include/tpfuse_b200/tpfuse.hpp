@@ -26,8 +26,13 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <memory>
+#include <optional>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -306,8 +311,75 @@ class RankEndpoint {
   tpf_comm* handle() { return c_; }
 
  private:
+  friend class SplitGroup;
+  explicit RankEndpoint(tpf_comm* adopted) : c_(adopted) {}
   tpf_comm* c_ = nullptr;
 };
+
+// ------------------------------------------- one GPU, the per-rank path (split group)
+// T endpoints built exactly like T processes' RankEndpoints (own symmetric heap, device epoch,
+// error record), peers mapped directly instead of through CUDA IPC (tpf_comm_create_split_group).
+// Device-level calls on every endpoint (any order, any threads, one stream) run as one launch
+// once the last rank has made its call; ep.sync() waits for that launch.
+class SplitGroup {
+ public:
+  explicit SplitGroup(int world, size_t sym_bytes) {
+    std::vector<tpf_comm*> cs(static_cast<size_t>(world), nullptr);
+    detail::check(tpf_comm_create_split_group(world, sym_bytes, cs.data()));
+    for (tpf_comm* c : cs) eps_.emplace_back(new RankEndpoint(c));
+  }
+  SplitGroup(const SplitGroup&) = delete;
+  SplitGroup& operator=(const SplitGroup&) = delete;
+  int size() const { return static_cast<int>(eps_.size()); }
+  RankEndpoint& endpoint(int r) { return *eps_.at(static_cast<size_t>(r)); }
+
+ private:
+  std::vector<std::unique_ptr<RankEndpoint>> eps_;
+};
+
+// spawn_group (fabric.hpp:185-226) over a split group: body(endpoint(r)) on one worker thread
+// per rank; results in rank order; the first failing rank is rethrown as GroupError naming it.
+template <typename Body>
+auto spawn_group(SplitGroup& group, Body&& body) {
+  using Result = std::invoke_result_t<Body&, RankEndpoint&>;
+  const int t = group.size();
+  std::vector<std::exception_ptr> errors(static_cast<size_t>(t));
+  std::vector<std::optional<std::conditional_t<std::is_void_v<Result>, int, Result>>> results(static_cast<size_t>(t));
+  std::vector<std::thread> workers;
+  for (int r = 0; r < t; ++r)
+    workers.emplace_back([&, r] {
+      try {
+        if constexpr (std::is_void_v<Result>) {
+          body(group.endpoint(r));
+          results[static_cast<size_t>(r)] = 0;
+        } else {
+          results[static_cast<size_t>(r)] = body(group.endpoint(r));
+        }
+      } catch (...) {
+        errors[static_cast<size_t>(r)] = std::current_exception();
+      }
+    });
+  for (std::thread& w : workers) w.join();
+  // A rank's GroupError already names the rank that failed (blame chain); any other failure
+  // names the rank that raised it.
+  for (int r = 0; r < t; ++r) {
+    if (!errors[static_cast<size_t>(r)]) continue;
+    try {
+      std::rethrow_exception(errors[static_cast<size_t>(r)]);
+    } catch (const GroupError&) {
+      throw;
+    } catch (const std::exception& e) {
+      throw GroupError(r, "rank " + std::to_string(r) + " failed: " + e.what());
+    }
+  }
+  if constexpr (std::is_void_v<Result>) {
+    return;
+  } else {
+    std::vector<Result> out;
+    for (auto& v : results) out.push_back(std::move(*v));
+    return out;
+  }
+}
 
 // Device-level drop-ins (layers.hpp:68-76). x/w bf16; out bf16 or fp32.
 inline void column_parallel_forward(RankEndpoint& ep, const DeviceTensor& x, const DeviceTensor& w_shard,

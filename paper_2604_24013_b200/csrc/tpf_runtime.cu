@@ -772,10 +772,21 @@ int tpf_comm_inject_fault(tpf_comm* c, int rank) {
 int tpf_comm_sync(tpf_comm* c, void* stream) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
   if (c->group) {
-    std::lock_guard<std::mutex> lock(c->group->mu);
-    if (c->group->npending > 0)
-      return fail(tpf::Status::invalid("split group: a collective call is still waiting for " +
-                                       std::to_string(c->world - c->group->npending) + " rank(s) to make it"));
+    // Ranks may run on their own threads (spawn_group): wait, bounded by the peer timeout, until
+    // every rank has made the pending call and the group launch has been issued.
+    const auto t0 = std::chrono::steady_clock::now();
+    while (true) {
+      int pending;
+      {
+        std::lock_guard<std::mutex> lock(c->group->mu);
+        pending = c->group->npending;
+      }
+      if (pending == 0) break;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(c->timeout_ns))
+        return fail(tpf::Status::invalid("split group: a collective call is still waiting for " +
+                                         std::to_string(c->world - pending) + " rank(s) to make it"));
+      std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
   }
   TPF_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   uint32_t rec[tpf::kErrWords];

@@ -210,7 +210,99 @@ static Tensor uniform_bf16(int64_t b, int64_t s, int64_t d, uint64_t seed) {
   return t;
 }
 
+// bf16 device copy of host values (all exactly representable: integer test data)
+static void* to_device_bf16(const std::vector<double>& v) {
+  std::vector<uint16_t> h(v.size());
+  for (size_t i = 0; i < v.size(); ++i) h[i] = detail::to_bf16(v[i]);
+  void* d = nullptr;
+  detail::cuda_check(cudaMalloc(&d, h.size() * 2), "cudaMalloc");
+  detail::cuda_check(cudaMemcpy(d, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "cudaMemcpy");
+  return d;
+}
+
+static Tensor from_device_f32(const void* d, int64_t b, int64_t s, int64_t n) {
+  std::vector<float> h(static_cast<size_t>(b * s * n));
+  detail::cuda_check(cudaMemcpy(h.data(), d, h.size() * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+  Tensor t(b, s, n);
+  for (size_t i = 0; i < h.size(); ++i) t.raw()[i] = h[i];
+  return t;
+}
+
+// The reference's threading model on the per-rank path: one worker thread per rank
+// (spawn_group), each calling the device-level drop-ins on its own RankEndpoint of a split group.
+static void split_group_tests() {
+  run("SplitGroup.SpawnGroupRowAndColumnParallelExact", [] {
+    const int t = 4, B = 1, S = 256, K = 128, N = 256;
+    const Tensor x = randint_fill(B, S, K, 0, 5, 31);
+    const Matrix wm = randint_matrix(K, N, -2, 2, 32);
+    const Tensor full = matmul(x, wm);
+    SplitGroup g(t, tpf_sym_bytes_rs(t, B, S, K / t, N, 1, TPF_F32) + tpf_sym_bytes_ag(t, B, S, K, N / t, 1));
+    const ShardedLinear rows = ShardedLinear::split_rows(wm, t), cols = ShardedLinear::split_columns(wm, t);
+    for (ScheduleKind k : {ScheduleKind::Ring, ScheduleKind::PairwiseBidirectional, ScheduleKind::CircularSlices}) {
+      const auto got = spawn_group(g, [&](RankEndpoint& ep) {
+        const int r = ep.rank();
+        DeviceTensor xd{to_device_bf16(feat_block(x, r * (K / t), K / t).raw()), B, S, K / t, TPF_BF16};
+        DeviceTensor wd{to_device_bf16(rows.shard(r).raw()), 1, K / t, N, TPF_BF16};
+        DeviceTensor yd{nullptr, B, S / t, N, TPF_F32};
+        detail::cuda_check(cudaMalloc(&yd.data, sizeof(float) * B * (S / t) * N), "cudaMalloc");
+        row_parallel_forward(ep, xd, wd, build_schedule(k, t), yd);
+        ep.sync();
+        Tensor y = from_device_f32(yd.data, B, S / t, N);
+        cudaFree(xd.data); cudaFree(wd.data); cudaFree(yd.data);
+        return y;
+      });
+      for (int r = 0; r < t; ++r) CHECK(got[r] == seq_slice(full, t, r));
+    }
+    const auto col = spawn_group(g, [&](RankEndpoint& ep) {
+      const int r = ep.rank();
+      DeviceTensor xd{to_device_bf16(seq_slice(x, t, r).raw()), B, S / t, K, TPF_BF16};
+      DeviceTensor wd{to_device_bf16(cols.shard(r).raw()), 1, K, N / t, TPF_BF16};
+      DeviceTensor yd{nullptr, B, S, N / t, TPF_F32};
+      detail::cuda_check(cudaMalloc(&yd.data, sizeof(float) * B * S * (N / t)), "cudaMalloc");
+      column_parallel_forward(ep, xd, wd, yd);
+      ep.sync();
+      Tensor y = from_device_f32(yd.data, B, S, N / t);
+      cudaFree(xd.data); cudaFree(wd.data); cudaFree(yd.data);
+      return y;
+    });
+    for (int r = 0; r < t; ++r) CHECK(col[r] == feat_block(full, r * (N / t), N / t));
+  });
+  // fabric_test.cpp:44-58: a failing rank surfaces as GroupError naming it
+  run("SplitGroup.SpawnGroupFailingRankIsNamed", [] {
+    const int t = 4, B = 1, S = 256, K = 128, N = 256;
+    SplitGroup g(t, tpf_sym_bytes_rs(t, B, S, K / t, N, 1, TPF_F32));
+    for (int r = 0; r < t; ++r) {
+      tpf_comm_set_timeout_ns(g.endpoint(r).handle(), 200ll * 1000 * 1000);
+      tpf_comm_inject_fault(g.endpoint(r).handle(), 2);
+    }
+    int failing = -1;
+    try {
+      spawn_group(g, [&](RankEndpoint& ep) {
+        DeviceTensor xd{nullptr, B, S, K / t, TPF_BF16}, wd{nullptr, 1, K / t, N, TPF_BF16},
+            yd{nullptr, B, S / t, N, TPF_F32};
+        cudaMalloc(&xd.data, 2 * B * S * (K / t));
+        cudaMemset(xd.data, 0, 2 * B * S * (K / t));
+        cudaMalloc(&wd.data, 2 * (K / t) * N);
+        cudaMemset(wd.data, 0, 2 * (K / t) * N);
+        cudaMalloc(&yd.data, 4 * B * (S / t) * N);
+        row_parallel_forward(ep, xd, wd, build_schedule(ScheduleKind::Ring, t), yd);
+        try {
+          ep.sync();
+        } catch (...) {
+          cudaFree(xd.data); cudaFree(wd.data); cudaFree(yd.data);
+          throw;
+        }
+        cudaFree(xd.data); cudaFree(wd.data); cudaFree(yd.data);
+      });
+    } catch (const GroupError& e) {
+      failing = e.failing_rank();
+    }
+    CHECK(failing == 2);
+  });
+}
+
 static void gpu_tests() {
+  split_group_tests();
   // SPEC acceptance C1: T in {1,2,4,8}, m in {1,2}, every applicable schedule, seeds 0-4,
   // B=2, S=64, D=32, hidden 64; exact equality with the single-device oracle.
   run("Acceptance.C1.ExactOracleEquivalence", [] {
