@@ -1,6 +1,6 @@
 """Per-GPU cost of one rank of a real TP group, at full-GPU scale (148 SMs), with virtual
-peers (Communicator.virtual_group: every peer wait passes at once, sends land in a scratch
-heap). It runs the real per-rank protocol instructions: wire reads and forwarding for AG,
+peers (Communicator.virtual_group: a self-ring -- the peers alias this rank's heap, so each
+send fills the slot this rank reads one step later and the step-to-step waits are real). It runs the real per-rank protocol instructions: wire reads and forwarding for AG,
 wire stores and inbox adds for RS, flag traffic. Compared against the same kernels in
 compute-only mode and against the plain T = 1 GEMM of the per-rank shape, this isolates the
 protocol's on-GPU overhead. NVLink latency is what it cannot show.
