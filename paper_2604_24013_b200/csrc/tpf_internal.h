@@ -34,6 +34,8 @@ enum Mode : int {
   MODE_SINGLE = 5,    // MODE_STD operands, T == 1 (no ring): the degenerate GEMM (+ epilogue act)
   MODE_QSPLIT = 6,    // GEMM-RS whose A slices are produced concurrently by the attention kernel:
                       // a step's tiles wait for their query slice's ready counter (Alg. 4)
+  MODE_RS_DIRECT = 7, // MODE_STD GEMM-RS with the pairwise schedule's rs_direct fold (its own
+                      // instance: the ring / circular MODE_STD instance carries no fold code)
 };
 
 // Blame table: a waiter that gives up on a peer flag (timeout, or the group aborting) records

@@ -298,6 +298,64 @@ __device__ __forceinline__ void rs_epilogue_fold(const KParams& p, uint32_t tadd
   if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_a);
 }
 
+// rs_direct last step of a pair's LAST tile (bf16 wire): the same fold, with the T-1 received
+// partials staged through shared memory by bulk copies. The fold reads T-1 partials per output
+// element; from L2 with per-thread loads it is latency-bound (~90 us for the final step at
+// TP = 8), while the pipeline stages are idle once the pair's last main loop is done. One elected
+// thread of the epilogue warpgroup copies sub-chunk j + 1 of every partial (T-1 contiguous
+// 8 KiB pieces) into one half of a double buffer while the group sums sub-chunk j from the
+// other half in the reference order ((c[p0] + c[p1]) + ...) and adds the own partial last.
+__device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t taddr, const char* in0, char* rp,
+                                                      int64_t ocol0, int row, bool valid, uint32_t tempty_a,
+                                                      uint8_t* sbuf, uint64_t* fbar, int eg, int ew) {
+  constexpr uint32_t kUnit = 4 * BM * 16;               // one 32-column sub-chunk of one bf16 partial
+  constexpr uint32_t kBuf = (kMaxRanks - 1) * kUnit;    // one half of the double buffer
+  const int nin = p.T - 1;
+  const bool issuer = ew == 0 && (threadIdx.x & 31) == 0;
+  auto issue = [&](int j) {
+    uint8_t* dst = sbuf + (j & 1) * kBuf;
+    mbar_arrive_expect_tx(fbar + (j & 1), nin * kUnit);
+    for (int s = 0; s < nin; ++s)
+      bulk_load(dst + s * kUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(j) * kUnit, kUnit, fbar + (j & 1));
+  };
+  // every warp of the group has acquired its rows' flags of all T-1 partials: the barrier carries
+  // those acquires to the issuer, whose proxy fence orders them before the async-proxy copies
+  named_bar_sync(1 + eg, 128);
+  if (issuer) {
+    fence_proxy_async_global();
+    issue(0);
+  }
+  for (int j = 0; j < BN / 32; ++j) {
+    if (issuer && j + 1 < BN / 32) issue(j + 1);
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + j * 32, r);
+    mbar_wait(p, fbar + (j & 1), (j >> 1) & 1);
+    tmem_ld_wait();
+    if (valid) {
+      const uint8_t* buf = sbuf + (j & 1) * kBuf;
+      float acc[32];
+#pragma unroll 1
+      for (int s = 0; s < nin; ++s) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          const uint4 w = *reinterpret_cast<const uint4*>(buf + s * kUnit + (g * BM + row) * 16);
+          const float in[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                               bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+#pragma unroll
+          for (int c = 0; c < 8; ++c) acc[g * 8 + c] = s == 0 ? in[c] : acc[g * 8 + c] + in[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = acc[c] + __uint_as_float(r[c]);
+      store_out_row(p, rp, ocol0 + j * 32, acc);
+    }
+    named_bar_sync(1 + eg, 128);  // half (j & 1) is read by every warp before sub-chunk j + 2 refills it
+  }
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_a);
+}
+
 // GEMM-RS epilogue of one 128 x 256 accumulator (this thread: one row), pipelined by one
 // 32-column sub-chunk: the inbox loads of sub-chunk j+1 are in flight while sub-chunk j is
 // read from TMEM, summed and stored (bf16 wire; the fp32 parity wire loads its inbox in
@@ -374,7 +432,8 @@ __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t
 // placement (after the prologue, after the last TMA load, implicit at exit), and it was
 // neutral on the fused AG-GEMM, so the multi-rank instances keep plain stream order.
 __host__ __device__ constexpr bool pdl_instance(int mode) {
-  return mode == MODE_SINGLE || mode == MODE_STD || mode == MODE_DP_GRAD || mode == MODE_GATHER_B;
+  return mode == MODE_SINGLE || mode == MODE_STD || mode == MODE_DP_GRAD || mode == MODE_GATHER_B ||
+         mode == MODE_RS_DIRECT;
 }
 
 // Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
@@ -390,6 +449,9 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   constexpr bool kUpEpi = kMode == MODE_PV;                            // merge_heads + push + flags
   constexpr bool kSingle = kMode == MODE_SINGLE;                       // T == 1: no ring at all
   constexpr bool kPdl = pdl_instance(kMode);                           // launched with PDL
+  // rs_direct (pairwise) fold: its own instance for MODE_STD operands; the DP / query-split
+  // instances keep the runtime switch
+  const bool direct = kMode == MODE_RS_DIRECT || (kMode != MODE_STD && p.direct);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -402,7 +464,8 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint64_t* tempty = bars + 2 * kStages + 2;  // leader: 8 epilogue warps of the pair
   // per CTA, per forwarder group: a forwarded A stage landed (MMA -> forwarder)
   uint64_t* fwd_ready = bars + 2 * kStages + 4;  // [2][kStages]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kStages + 4);
+  uint64_t* fold_bar = bars + 4 * kStages + 4;   // [2]: rs_direct fold staging (double buffer)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kStages + 6);
 
   // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -439,6 +502,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 8);
+      mbar_init(fold_bar + a, 1);
     }
     fence_barrier_init();
   }
@@ -919,7 +983,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       const int slot_send = pass * (p.T - 1) + it;
       const int send_rank = p.T > 1 ? p.sched[rank][it][0] : -1;
       const char* inbox = nullptr;
-      if (tile_live && !p.direct && it > 0 && !p.compute_only) {
+      if (tile_live && !direct && it > 0 && !p.compute_only) {
         const int slot_in = slot_send - 1;
         const uint64_t tw0 = (p.trace && lane == 0) ? globaltimer() : 0;
         const uint32_t* fin = flag_ptr(p, par, rank, slot_in, fidx);
@@ -931,7 +995,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         }
         inbox = slot_ptr(p, par, rank, slot_in) + tile_idx * tile_bytes;
       }
-      if (tile_live && p.direct && last && p.T > 1 && !p.compute_only) {
+      if (tile_live && direct && last && p.T > 1 && !p.compute_only) {
         publish();
         for (int s = 0; s < p.T - 1; ++s)
           wait_flag(p, flag_ptr(p, par, rank, pass * (p.T - 1) + s, fidx), rank, p.sched[rank][s][1], t.step, lin,
@@ -946,11 +1010,16 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       const int64_t ocol = kUpEpi ? p.out_col_off[h] + (hm ? static_cast<int64_t>(t.b % hm) * p.N : 0) : 0;
       const int64_t orow = ob * p.out_rows + pass * p.Sc + t.row0 + row;
       char* rp = ((kUpEpi && p.out_rank[h]) ? p.out_rank[h] : out_h) + (orow * p.out_ld + ocol) * esz;
-      const bool folding = p.direct && last && p.T > 1 && !p.compute_only;
+      const bool folding = direct && last && p.T > 1 && !p.compute_only;
       if (folding) {
         const char* in0 = slot_ptr(p, par, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
-        rs_epilogue_fold(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
-                         a ? tempty_leader1 : tempty_leader0);
+        // the pair's last tile: its main loops are done, so the pipeline stages stage the fold
+        if (kMode == MODE_RS_DIRECT && !p.wire_f32 && tile_live && lin + GP >= ntiles)
+          rs_epilogue_fold_smem(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
+                                a ? tempty_leader1 : tempty_leader0, smem, fold_bar, eg, ew);
+        else
+          rs_epilogue_fold(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
+                           a ? tempty_leader1 : tempty_leader0);
       } else {
         // Software-pipelined by one 32-column sub-chunk: the TMEM read and the inbox loads
         // of sub-chunk j+1 are in flight while sub-chunk j is summed and stored, so each
@@ -1101,6 +1170,7 @@ cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream) {
     case MODE_QK: return launch_instance<OP_RS, MODE_QK>(p, grid, stream);
     case MODE_PV: return launch_instance<OP_RS, MODE_PV>(p, grid, stream);
     case MODE_QSPLIT: return launch_instance<OP_RS, MODE_QSPLIT>(p, grid, stream);
+    case MODE_RS_DIRECT: return launch_instance<OP_RS, MODE_RS_DIRECT>(p, grid, stream);
     case MODE_SINGLE:
       return p.op == OP_AG ? launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream)
                            : launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);
@@ -1117,6 +1187,7 @@ cudaError_t launch_fused_group(const GroupParams& gp, int grid, cudaStream_t str
                                  : launch_instance<OP_RS, MODE_STD>(gp, grid, stream);
     case MODE_DP_GRAD: return launch_instance<OP_RS, MODE_DP_GRAD>(gp, grid, stream);
     case MODE_GATHER_B: return launch_instance<OP_AG, MODE_GATHER_B>(gp, grid, stream);
+    case MODE_RS_DIRECT: return launch_instance<OP_RS, MODE_RS_DIRECT>(gp, grid, stream);
     default: return cudaErrorInvalidValue;  // other instances are not split-group operations
   }
 }

@@ -252,6 +252,10 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 }
 
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+// Named barrier among `threads` threads (ids 1..15; 0 is __syncthreads).
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
 
 // Group abort (tpf::Blame): word `abort_word` of all T ranks' tables := the aborted call's epoch
 // (the ranks of a group advance their epochs in lockstep, so a stale abort of an earlier call
