@@ -1,6 +1,6 @@
 """Regenerate the committed SASS evidence from the built library (no GPU needed):
     python profiles/sass_summary.py
-writes profiles/r01_sass_tpfuse_b200.txt (full listing) and profiles/r01_sass_summary.txt
+writes profiles/<tag>_sass_tpfuse_b200.txt (full listing; committed gzipped) and profiles/<tag>_sass_summary.txt
 (per-kernel counts of the tcgen05 / TMA / TMEM / peer-store / fence mnemonics)."""
 import collections
 import os
