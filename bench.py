@@ -533,6 +533,11 @@ def virtual_block(args, dev, stream, T):
     t_roof_ag = max(fl_ag / pk, rows_moved * D_MODEL * 2 / 900e9) * 1e3
     t_roof_rs = max(fl_rs / pk, rows_moved * D_MODEL * 2 / 900e9) * 1e3
     t_roof_rs32 = max(fl_rs / pk, rows_moved * D_MODEL * 4 / 900e9) * 1e3
+    # the same with the pool's measured peer-copy rate, 770 GB/s per direction
+    # (/opt/skills/guides/B200_PROFILING.md): the RS bf16 wire is then link-bound at TP = 8
+    m_ag = max(fl_ag / pk, rows_moved * D_MODEL * 2 / 770e9) * 1e3
+    m_rs = max(fl_rs / pk, rows_moved * D_MODEL * 2 / 770e9) * 1e3
+    m_rs32 = max(fl_rs / pk, rows_moved * D_MODEL * 4 / 770e9) * 1e3
     return {"tp": T, "note": "one GPU of a TP group at full scale: rank 0 with virtual peers (self-ring: "
                              "peers alias the own heap, sends fill the slot read one step later, zero link "
                              "latency); medians of 5 rounds of 20 back-to-back calls per op; plain = the T = 1 "
@@ -543,9 +548,13 @@ def virtual_block(args, dev, stream, T):
             "exposed_comm_us": {"ag": 1e3 * (m["ag"] - m["p_ag"]), "rs": 1e3 * (m["rs"] - m["p_rs"])},
             "tail_us": {"ag": tail_ag, "rs": tail_rs},
             "ag_tflops_per_gpu": fl_ag / (m["ag"] * 1e-3) / 1e12, "rs_tflops_per_gpu": fl_rs / (m["rs"] * 1e-3) / 1e12,
-            "t_roof_ms": {"ag": t_roof_ag, "rs": t_roof_rs, "rs_f32_wire": t_roof_rs32},
+            "t_roof_ms": {"ag": t_roof_ag, "rs": t_roof_rs, "rs_f32_wire": t_roof_rs32,
+                          "how": "max(FLOPs at the measured bf16 burst peak, NVLink bytes at 900 GB/s) (north_star)"},
             "frac_of_t_roof": {"ag": t_roof_ag / m["ag"], "rs": t_roof_rs / m["rs"],
-                               "rs_f32_wire": t_roof_rs32 / m["rs32"]}}
+                               "rs_f32_wire": t_roof_rs32 / m["rs32"]},
+            "t_roof_ms_link770": {"ag": m_ag, "rs": m_rs, "rs_f32_wire": m_rs32,
+                                  "how": "NVLink at the measured 770 GB/s peer copy (profiling guide)"},
+            "frac_of_t_roof_link770": {"ag": m_ag / m["ag"], "rs": m_rs / m["rs"], "rs_f32_wire": m_rs32 / m["rs32"]}}
 
 
 # ------------------------------------------------------------- launch / dry run
