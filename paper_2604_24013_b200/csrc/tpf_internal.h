@@ -21,6 +21,14 @@ constexpr int kAStageBytes = BM * BK * 2;        // 16 KiB: also the AG wire "im
 constexpr int kBStageBytes = (BN / 2) * BK * 2;  // 16 KiB: this CTA's half of B
 constexpr int kStageBytes = kAStageBytes + kBStageBytes;
 constexpr int kSmemBytes = kStages * kStageBytes + 1024 + 512;  // + barriers
+// Pairwise (MODE_RS_DIRECT) instance: one pipeline stage fewer, and behind the barriers a fold
+// staging area per epilogue warpgroup (two buffers of T-1 <= 7 partials x one 16-B word column
+// = 128 rows x 16 B = 2 KiB each).
+constexpr int kStagesDirect = kStages - 1;
+constexpr int kFoldUnit = BM * 16;                                  // 2 KiB
+constexpr int kFoldGroupBytes = 2 * (kMaxRanks - 1) * kFoldUnit;    // 28 KiB per warpgroup
+constexpr int kSmemBytesDirect = kStagesDirect * kStageBytes + 2048 + 2 * kFoldGroupBytes + 1024;
+static_assert(kSmemBytesDirect <= 227 * 1024, "pairwise instance exceeds the shared-memory limit");
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
 enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };

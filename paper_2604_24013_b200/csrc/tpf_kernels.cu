@@ -305,7 +305,7 @@ __device__ __forceinline__ void rs_epilogue_fold(const KParams& p, uint32_t tadd
 // thread of the epilogue warpgroup copies sub-chunk j + 1 of every partial (T-1 contiguous
 // 8 KiB pieces) into one half of a double buffer while the group sums sub-chunk j from the
 // other half in the reference order ((c[p0] + c[p1]) + ...) and adds the own partial last.
-__device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t taddr, const char* in0, char* rp,
+__device__ __noinline__ void rs_epilogue_fold_stages(const KParams& p, uint32_t taddr, const char* in0, char* rp,
                                                       int64_t ocol0, int row, bool valid, uint32_t tempty_a,
                                                       uint8_t* sbuf, uint64_t* fbar, int eg, int ew) {
   constexpr uint32_t kUnit = 4 * BM * 16;               // one 32-column sub-chunk of one bf16 partial
@@ -350,6 +350,65 @@ __device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t ta
       store_out_row(p, rp, ocol0 + j * 32, acc);
     }
     named_bar_sync(1 + eg, 128);  // half (j & 1) is read by every warp before sub-chunk j + 2 refills it
+  }
+  tc_fence_before();
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) mbar_arrive_cluster(tempty_a);
+}
+
+// rs_direct last step, bf16 wire (MODE_RS_DIRECT): the fold reads T-1 partials per output
+// element, which from L2 with per-thread loads is latency-bound (a traced cfg2 TP8 call spent
+// ~90 us folding after its last main loop). Instead one elected thread of the epilogue warpgroup
+// bulk-copies the T-1 partials' next 8-column word (T-1 contiguous 2 KiB pieces of the wire
+// images) into one half of the group's double buffer while the group sums the current word from
+// the other half, in the reference order ((c[p0] + c[p1]) + ...), and adds the own partial last.
+__device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t taddr, const char* in0, char* rp,
+                                                   int64_t ocol0, int row, bool valid, uint32_t tempty_a,
+                                                   uint8_t* sbuf, uint64_t* fbar, int eg, int ew) {
+  constexpr uint32_t kBuf = (kMaxRanks - 1) * kFoldUnit;  // one half of the double buffer
+  constexpr int kWords = BN / 8;                           // 16-B words (8 bf16 columns) per row
+  const int nin = p.T - 1;
+  const bool issuer = ew == 0 && (threadIdx.x & 31) == 0;
+  // word u of every partial: wire_off(0, u / 4, u % 4, 0) = u * BM * 16
+  auto issue = [&](int u) {
+    uint8_t* dst = sbuf + (u & 1) * kBuf;
+    mbar_arrive_expect_tx(fbar + (u & 1), nin * kFoldUnit);
+    for (int s = 0; s < nin; ++s)
+      bulk_load(dst + s * kFoldUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(u) * kFoldUnit, kFoldUnit,
+                fbar + (u & 1));
+  };
+  // every warp of the group has acquired its rows' flags of all T-1 partials: the barrier carries
+  // those acquires to the issuer, whose proxy fence orders them before the async-proxy copies
+  named_bar_sync(1 + eg, 128);
+  if (issuer) {
+    fence_proxy_async_global();
+    issue(0);
+  }
+  for (int j = 0; j < BN / 32; ++j) {
+    uint32_t r[32];
+    tmem_ld_32x32b_x32(taddr + j * 32, r);
+    float v[32];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int u = j * 4 + g;
+      if (issuer && u + 1 < kWords) issue(u + 1);
+      mbar_wait(p, fbar + (u & 1), (u >> 1) & 1);
+      if (g == 0) tmem_ld_wait();
+      const uint8_t* buf = sbuf + (u & 1) * kBuf;
+      float acc[8];
+#pragma unroll 1
+      for (int s = 0; s < nin; ++s) {
+        const uint4 w = *reinterpret_cast<const uint4*>(buf + s * kFoldUnit + row * 16);
+        const float in[8] = {bf16lo(w.x), bf16hi(w.x), bf16lo(w.y), bf16hi(w.y),
+                             bf16lo(w.z), bf16hi(w.z), bf16lo(w.w), bf16hi(w.w)};
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[c] = s == 0 ? in[c] : acc[c] + in[c];
+      }
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[g * 8 + c] = acc[c] + __uint_as_float(r[g * 8 + c]);
+      named_bar_sync(1 + eg, 128);  // half (u & 1) is read by every warp before word u + 2 refills it
+    }
+    if (valid) store_out_row(p, rp, ocol0 + j * 32, v);
   }
   tc_fence_before();
   __syncwarp();
@@ -456,16 +515,18 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
-  uint8_t* smem_b = smem + kStages * kAStageBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  constexpr int kSt = kMode == MODE_RS_DIRECT ? kStagesDirect : kStages;  // pipeline stages
+  uint8_t* smem_b = smem + kSt * kAStageBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes);
   uint64_t* full = bars;                  // leader: 2 arrivals + 2 x stage tx bytes
-  uint64_t* empty = bars + kStages;       // per CTA: 1 (leader's multicast commit)
-  uint64_t* tfull = bars + 2 * kStages;   // per CTA: 1 (leader's multicast commit)
-  uint64_t* tempty = bars + 2 * kStages + 2;  // leader: 8 epilogue warps of the pair
+  uint64_t* empty = bars + kSt;       // per CTA: 1 (leader's multicast commit)
+  uint64_t* tfull = bars + 2 * kSt;   // per CTA: 1 (leader's multicast commit)
+  uint64_t* tempty = bars + 2 * kSt + 2;  // leader: 8 epilogue warps of the pair
   // per CTA, per forwarder group: a forwarded A stage landed (MMA -> forwarder)
-  uint64_t* fwd_ready = bars + 2 * kStages + 4;  // [2][kStages]
-  uint64_t* fold_bar = bars + 4 * kStages + 4;   // [2]: rs_direct fold staging (double buffer)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kStages + 6);
+  uint64_t* fwd_ready = bars + 2 * kSt + 4;  // [2][kSt]
+  uint64_t* fold_bar = bars + 4 * kSt + 4;   // [2 groups][2 buffers]: rs_direct fold staging
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kSt + 8);
+  uint8_t* fold_smem = smem + kSt * kStageBytes + 2048;  // MODE_RS_DIRECT: [2 groups][kFoldGroupBytes]
 
   // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -493,16 +554,17 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
     }
   }
   if (warp == 1 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < kSt; ++s) {
       mbar_init(full + s, 2);
       mbar_init(empty + s, (fwd && kGatherB) ? 2 : 1);
       mbar_init(fwd_ready + s, 1);
-      mbar_init(fwd_ready + kStages + s, 1);
+      mbar_init(fwd_ready + kSt + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 8);
       mbar_init(fold_bar + a, 1);
+      mbar_init(fold_bar + 2 + a, 1);
     }
     fence_barrier_init();
   }
@@ -671,7 +733,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             }
             if (p.trace && kb == 0) t_first = globaltimer();
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == kSt) { stage = 0; phase ^= 1; }
         }
         if (p.trace && lane == 0) trace_rec(p, TR_MAINLOOP, rank, t.step, lin, t_first, globaltimer());
       }
@@ -702,7 +764,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             mbar_wait(p, full + stage, phase);
             tc_fence_after();
             if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
-              uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kStages + stage;
+              uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kSt + stage;
               mbar_arrive(fr);
               mbar_arrive_cluster(mapa_shared(smem_u32(fr), 1));
               ++fo;
@@ -722,7 +784,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
               mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
             mma_commit_2sm(empty + stage, 0x3);
-            if (++stage == kStages) { stage = 0; phase ^= 1; }
+            if (++stage == kSt) { stage = 0; phase ^= 1; }
           }
           mma_commit_2sm(tfull + a, 0x3);
         }
@@ -857,8 +919,8 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             const bool batch_end = (fo % fbatch) == fbatch - 1;
             ++fo;
             if (!mine) continue;
-            const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kStages);
-            mbar_wait(p, fwd_ready + grp * kStages + stage, (ph >> stage) & 1u);
+            const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kSt);
+            mbar_wait(p, fwd_ready + grp * kSt + stage, (ph >> stage) & 1u);
             ph ^= 1u << stage;
             if (live) {
               const int64_t img = img0 + kb;
@@ -1013,10 +1075,16 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       const bool folding = direct && last && p.T > 1 && !p.compute_only;
       if (folding) {
         const char* in0 = slot_ptr(p, par, rank, pass * (p.T - 1)) + tile_idx * tile_bytes;
-        // the pair's last tile: its main loops are done, so the pipeline stages stage the fold
+        // pairwise instance, bf16 wire: stage the fold through shared memory -- the pair's last
+        // tile through its idle pipeline stages (8 KiB pieces, 32 columns at a time), every other
+        // fold tile through the warpgroup's own buffers (2 KiB pieces, 8 columns at a time)
         if (kMode == MODE_RS_DIRECT && !p.wire_f32 && tile_live && lin + GP >= ntiles)
+          rs_epilogue_fold_stages(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
+                                  a ? tempty_leader1 : tempty_leader0, smem, fold_bar + 2 * eg, eg, ew);
+        else if (kMode == MODE_RS_DIRECT && !p.wire_f32 && tile_live)
           rs_epilogue_fold_smem(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
-                                a ? tempty_leader1 : tempty_leader0, smem, fold_bar, eg, ew);
+                                a ? tempty_leader1 : tempty_leader0, fold_smem + eg * kFoldGroupBytes,
+                                fold_bar + 2 * eg, eg, ew);
         else
           rs_epilogue_fold(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
                            a ? tempty_leader1 : tempty_leader0);
@@ -1119,8 +1187,9 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
     kern = tpf_fused_kernel<kOp, kMode>;
   static uint64_t attr_done = 0;
   static bool pool_ok[64];
+  constexpr int kSmem = kMode == MODE_RS_DIRECT ? kSmemBytesDirect : kSmemBytes;
   once_per_device(attr_done, [kern] {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     // the setmaxnreg split must fit the register pool the launch allocates, or
     // setmaxnreg.inc blocks forever
     cudaFuncAttributes fa;
@@ -1137,7 +1206,7 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for tcgen05 cta_group::2
