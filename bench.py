@@ -421,6 +421,9 @@ def run_ours(args, rank, world, local_rank):
     virt = None
     if world == 1 and args.emulate_tp > 1:
         virt = virtual_block(args, dev, stream, args.emulate_tp)
+    others = None
+    if world == 1 and args.emulate_tp > 1 and not args.no_other_configs:
+        others = other_configs_block(dev, stream)
 
     comm.close()
     if rank != 0:
@@ -479,7 +482,89 @@ def run_ours(args, rank, world, local_rank):
         out["baseline_cublas_nccl"] = base
     if virt:
         out["virtual_per_gpu"] = virt
+    if others:
+        out["other_configs"] = others
     print(json.dumps(out))
+
+
+def other_configs_block(dev, stream):
+    """The other BASELINE configurations, measured in the same run (informational; the headline
+    is cfg2): one GPU of a TP = 8 group (virtual peers) on the cfg3 attention projections, one
+    GPU of the 8-rank DP group of cfg4, and the cfg5 UP layer (all 8 ranks on this GPU, each on
+    148/8 SMs). Fused vs plain per-rank GEMM; medians of 3 alternating rounds."""
+    import statistics
+
+    import torch
+
+    import paper_2604_24013_b200 as tpf
+    pk = peaks()["bf16_tflops"] * 1e12
+    one = tpf.Communicator.create(0, 1, 0)
+    g = torch.Generator(device=dev).manual_seed(21)
+    res = {}
+
+    def pair(fused, plain, rounds=3):
+        for _ in range(2):
+            fused(); plain()
+        f, q = [], []
+        for _ in range(rounds):
+            f.append(_timed_calls(fused, stream, 10))
+            q.append(_timed_calls(plain, stream, 10))
+        return statistics.median(f), statistics.median(q)
+
+    def row(fms, pms, flops, wire):
+        roof = max(flops / pk, wire / 900e9) * 1e3
+        return {"fused_ms": fms, "plain_gemm_ms": pms, "fused_over_plain": fms / pms,
+                "exposed_us": 1e3 * (fms - pms), "tflops": flops / (fms * 1e-3) / 1e12,
+                "t_roof_ms": roof, "frac_of_t_roof": roof / fms}
+
+    T, S, K = 8, 16384, 8192
+    x = torch.randn((1, S // T, K), device=dev, generator=g).to(torch.bfloat16)
+    xg = torch.randn((1, S, K), device=dev, generator=g).to(torch.bfloat16)
+    wq = (torch.randn((K, 10240 // T), device=dev, generator=g) / 90).to(torch.bfloat16)
+    yq = torch.empty((1, S, 10240 // T), device=dev, dtype=torch.bfloat16)
+    xo = torch.randn((1, S, K // T), device=dev, generator=g).to(torch.bfloat16)
+    wo = (torch.randn((K // T, K), device=dev, generator=g) / 90).to(torch.bfloat16)
+    yo = torch.empty((1, S // T, K), device=dev, dtype=torch.bfloat16)
+    yog = torch.empty((1, S, K), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, K, 10240 // T),
+                                                 tpf.sym_bytes_rs(T, 1, S, K // T, K, 1, tpf.BF16)))
+    fq, pq = pair(lambda: comm.ag_gemm(x, wq, yq, stream=stream), lambda: one.ag_gemm(xg, wq, yq, stream=stream))
+    fo, po = pair(lambda: comm.gemm_rs(xo, wo, yo, kind=tpf.RING, wire=tpf.BF16, stream=stream),
+                  lambda: one.gemm_rs(xo, wo, yog, stream=stream))
+    comm.sync(stream)
+    comm.close()
+    moved = (T - 1) / T * S * 2
+    res["cfg3_tp8_per_gpu"] = {"qkv_ag_gemm": row(fq, pq, 2.0 * S * K * 10240 / T, moved * K),
+                               "out_proj_gemm_rs_bf16_wire": row(fo, po, 2.0 * S * K * K / T, moved * K)}
+    del x, xg, wq, yq, xo, wo, yo, yog
+    M, K4, N4 = 4096, 2048, 8192
+    X = torch.randn((M, K4), device=dev, generator=g).to(torch.bfloat16)
+    dY = (torch.randn((M, N4), device=dev, generator=g) / 64).to(torch.bfloat16)
+    dW = torch.empty((K4 // T, N4), device=dev, dtype=torch.bfloat16)
+    dWf = torch.empty((K4, N4), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.virtual_group(T, tpf.sym_bytes_rs(T, 1, K4, M, N4, 1, tpf.BF16))
+    fd, pd = pair(lambda: comm.dp_grad_rs(X, dY, dW, kind=tpf.RING, wire=tpf.BF16, stream=stream),
+                  lambda: one.dp_grad_rs(X, dY, dWf, stream=stream))
+    comm.sync(stream)
+    comm.close()
+    res["cfg4_dp8_per_gpu"] = {"grad_rs_bf16_wire": row(fd, pd, 2.0 * M * K4 * N4, (T - 1) / T * K4 * N4 * 2),
+                               "shape": "4096 tokens / rank, 2048 x 8192 weight"}
+    del X, dY, dW, dWf
+    heads, S5 = 4, 32768
+    q, k, v = (torch.randn((T, heads, S5, 128), device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o = torch.empty((T, 1, S5 // T, T * heads * 128), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_ulysses(T, 1, T * heads, S5, 128))
+    up = lambda: comm.attention_a2a(q, k, v, o, 1, heads, stream=stream)  # noqa: E731
+    up()
+    ms = statistics.median(_timed_calls(up, stream, 2) for _ in range(3))
+    comm.sync(stream)
+    comm.close()
+    res["cfg5_up_attention_local_group"] = {
+        "ms": ms, "tflops": 4.0 * T * heads * S5 * S5 * 128 / (ms * 1e-3) / 1e12,
+        "note": "fuse_all_to_all_attention, T = 8 ranks on this GPU (each on 148/8 SMs), 4 heads x 128 per "
+                "rank, S = 32768, non-causal; the output all-to-all is fused in the epilogue"}
+    one.close()
+    return res
 
 
 def virtual_block(args, dev, stream, T):
@@ -601,6 +686,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--emulate-tp", type=int, default=8, help="per-GPU TP group model at N=1 (0 = off)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU reference sample")
+    ap.add_argument("--no-other-configs", action="store_true", help="skip the cfg3 / cfg4 / cfg5 block (N=1)")
     ap.add_argument("--dry-run", action="store_true", help="launcher / rank plumbing only (gloo, no GPU)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
