@@ -29,6 +29,10 @@ constexpr int kFoldUnit = BM * 16;                                  // 2 KiB
 constexpr int kFoldGroupBytes = 2 * (kMaxRanks - 1) * kFoldUnit;    // 28 KiB per warpgroup
 constexpr int kSmemBytesDirect = kStagesDirect * kStageBytes + 2048 + 2 * kFoldGroupBytes + 1024;
 static_assert(kSmemBytesDirect <= 227 * 1024, "pairwise instance exceeds the shared-memory limit");
+// A-carrying AG-GEMM (MODE_STD): two 16 KiB forwarder bounce buffers after 1 KiB of barriers
+// (+ 1 KiB alignment slack; the kernel's 1 KiB of static shared memory counts against 227 KiB)
+constexpr int kSmemBytesFwd = kStages * kStageBytes + 1024 + 2 * kAStageBytes + 1024;
+static_assert(kSmemBytesFwd + 1024 <= 227 * 1024, "AG instance exceeds the shared-memory limit");
 
 enum Op : int { OP_RS = 0, OP_AG = 1 };
 enum Act : int { ACT_NONE = 0, ACT_SQUARE = 1, ACT_SWIGLU = 2 };

@@ -526,7 +526,9 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint64_t* fwd_ready = bars + 2 * kSt + 4;  // [2][kSt]
   uint64_t* fold_bar = bars + 4 * kSt + 4;   // [2 groups][2 buffers]: rs_direct fold staging
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kSt + 8);
+  uint64_t* fwd_bar = bars + 4 * kSt + 9;    // [2]: A-carrying AG forwarder bulk loads
   uint8_t* fold_smem = smem + kSt * kStageBytes + 2048;  // MODE_RS_DIRECT: [2 groups][kFoldGroupBytes]
+  uint8_t* fwd_smem = smem + kSt * kStageBytes + 1024;   // A-carrying AG: 2 x 16 KiB forwarder buffers
 
   // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -565,6 +567,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       mbar_init(tempty + a, 8);
       mbar_init(fold_bar + a, 1);
       mbar_init(fold_bar + 2 + a, 1);
+      mbar_init(fwd_bar + a, 1);
     }
     fence_barrier_init();
   }
@@ -794,7 +797,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       if (fwd && !kGatherB) {
         // A-carrying AG: the ring forward is decoupled from the GEMM. Every CTA's two
         // forwarder warps take a share of each step's images (round-robin over all CTAs of
-        // the rank), step by step: step 0 copies from x (row-major, swizzled here into the
+        // the rank), step by step: step 0 copies from x (a tensor load puts the rows in the
         // SW128 image layout, zero past K), step i > 0 copies the inbox image of slot i-1
         // once the predecessor's flag is seen, into the successor's slot i. No pipeline
         // stage is ever held (gating stage reuse on a forwarder cost 10-18 us per call at
@@ -803,19 +806,30 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         // on it. Each warp fences and publishes its flags per batch and at every step end.
         const int fw = g * 2 + (warp - 2);  // this warp's index among the rank's forwarders
         const int nfw = G * 2;
+        // Copies are TMA bulk operations issued by lane 0 through a 16 KiB SMEM bounce buffer
+        // per warp: a load into the buffer, then a bulk store into the successor's slot. No
+        // registers hold data, so the copy rate is not bounded by the loads in flight that the
+        // 88-register control warps can hold (cfg3 TP8 per-GPU AG 308 -> 300 us, wire waits
+        // 966 -> 218 per call).
+        uint8_t* fbuf = fwd_smem + (warp - 2) * kAStageBytes;
+        uint64_t* fbar = fwd_bar + (warp - 2);
+        uint32_t fph = 0;
         int unpub[8];  // fbatch <= 8
         int nunpub = 0;
         int cur_slot = 0, cur_dst = 0;
         auto flush = [&]() {
           const uint64_t tf0 = p.trace ? globaltimer() : 0;
-          fence_sys();
+          if (lane == 0) {
+            bulk_wait<0>();               // this warp's bulk stores have completed
+            fence_proxy_async_global();   // ... ordered before the generic flag stores
+            fence_sys();
+            if (rank != p.fault_rank)
+              for (int i = 0; i < nunpub; ++i) st_relaxed_sys(flag_ptr(p, par, cur_dst, cur_slot, unpub[i]), ep);
+          }
           __syncwarp();
-          if (lane == 0 && rank != p.fault_rank)
-            for (int i = 0; i < nunpub; ++i) st_relaxed_sys(flag_ptr(p, par, cur_dst, cur_slot, unpub[i]), ep);
           if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
           nunpub = 0;
         };
-        const char* xh = p.x + h * p.x_rank_stride;
         const int nimg = p.nmb * p.nkb;
         for (int pass = 0; pass < p.m; ++pass) {
           for (int it = 0; it < p.T - 1; ++it) {
@@ -827,49 +841,28 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
               const int mb = img / p.nkb, kb = img - mb * p.nkb;
               const int bb = mb / p.nmb_per_batch, j = mb - bb * p.nmb_per_batch;
               const int row0 = j * BM;
-              const int valid = static_cast<int>(min(static_cast<int64_t>(BM), p.Sc - row0));
-              if (valid <= 0) continue;  // padding m-block of an odd pair: never read
-              char* dst = slot_ptr(p, par, cur_dst, slot) + static_cast<int64_t>(img) * kAStageBytes;
-              if (it == 0) {
-                // lane owns 16-B chunk c = lane & 7 of rows (lane >> 3) + 4 * i; SW128: chunk c
-                // of row r sits at r * 128 + ((c ^ (r & 7)) << 4)
-                const int c = lane & 7, r0 = lane >> 3;
-                const int64_t col = static_cast<int64_t>(kb) * BK + c * 8;
-                const bool col_ok = col < p.K;
-                const char* xs =
-                    xh + ((static_cast<int64_t>(bb) * p.x_rows + pass * p.Sc + row0 + r0) * p.K + col) * 2;
-                const int64_t xstep = static_cast<int64_t>(4) * p.K * 2;  // 4 rows
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  uint4 v[8];
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) {
-                    const int r = r0 + 4 * (q * 8 + i);
-                    v[i] = (col_ok && r < valid) ? *reinterpret_cast<const uint4*>(xs + (q * 8 + i) * xstep)
-                                                 : make_uint4(0u, 0u, 0u, 0u);
-                  }
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) {
-                    const int r = r0 + 4 * (q * 8 + i);
-                    *reinterpret_cast<uint4*>(dst + r * 128 + ((c ^ (r & 7)) << 4)) = v[i];
-                  }
+              if (p.Sc - row0 <= 0) continue;  // padding m-block of an odd pair: never read
+              if (lane == 0) {
+                char* dst = slot_ptr(p, par, cur_dst, slot) + static_cast<int64_t>(img) * kAStageBytes;
+                bulk_wait_read<0>();  // the previous store has read the buffer
+                if (it == 0) {
+                  // rows past this chunk are read as whatever x holds there (their products
+                  // are never stored)
+                  mbar_arrive_expect_tx(fbar, kAStageBytes);
+                  tma_load_4d(fbuf, &p.tmap_a, fbar, kb * BK, pass * static_cast<int>(p.Sc) + row0, bb, h);
+                } else {
+                  const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
+                  wait_flag(p, fsrc, rank, p.sched[rank][it - 1][1], pass * p.T + it, img, ep);
+                  fence_proxy_async_global();  // the acquired image, read by the async proxy
+                  mbar_arrive_expect_tx(fbar, kAStageBytes);
+                  bulk_load(fbuf, slot_ptr(p, par, rank, slot - 1) + static_cast<int64_t>(img) * kAStageBytes,
+                            kAStageBytes, fbar);
                 }
-              } else {
-                const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
-                if (lane == 0) wait_flag(p, fsrc, rank, p.sched[rank][it - 1][1], pass * p.T + it, img, ep);
-                __syncwarp();
-                (void)ld_acquire_sys(fsrc);  // every lane reads the image after the flag
-                const uint4* src =
-                    reinterpret_cast<const uint4*>(slot_ptr(p, par, rank, slot - 1) + static_cast<int64_t>(img) * kAStageBytes);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  uint4 v[8];
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) v[i] = src[(q * 8 + i) * 32 + lane];
-#pragma unroll
-                  for (int i = 0; i < 8; ++i) reinterpret_cast<uint4*>(dst)[(q * 8 + i) * 32 + lane] = v[i];
-                }
+                mbar_wait(p, fbar, fph);
+                bulk_store(dst, fbuf, kAStageBytes);
+                bulk_commit();
               }
+              fph ^= 1;
               unpub[nunpub++] = img;
               if (nunpub == fbatch) flush();
             }
@@ -1187,7 +1180,9 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
     kern = tpf_fused_kernel<kOp, kMode>;
   static uint64_t attr_done = 0;
   static bool pool_ok[64];
-  constexpr int kSmem = kMode == MODE_RS_DIRECT ? kSmemBytesDirect : kSmemBytes;
+  constexpr int kSmem = kMode == MODE_RS_DIRECT                        ? kSmemBytesDirect
+                        : (kOp == OP_AG && kMode == MODE_STD) ? kSmemBytesFwd
+                                                              : kSmemBytes;
   once_per_device(attr_done, [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     // the setmaxnreg split must fit the register pool the launch allocates, or
