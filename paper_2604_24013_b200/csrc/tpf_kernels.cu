@@ -420,32 +420,31 @@ __device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t ta
 // read from TMEM, summed and stored (bf16 wire; the fp32 parity wire loads its inbox in
 // the same iteration). The accumulator is released as soon as its last columns are in
 // registers. kF32 is a template parameter so each instance keeps only its own buffers live.
-template <bool kF32>
+template <bool kF32, int kDepth>
 __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t taddr, const char* inbox,
                                                       char* dst_tile, char* rp, int64_t ocol0, int row,
                                                       bool valid, bool last, uint32_t tempty_a) {
   constexpr int kW = kF32 ? 8 : 4;  // 16-B inbox words per sub-chunk
   constexpr int kNJ = BN / 32;
-  constexpr bool kAhead = !kF32;
+  // bf16 wire: kDepth sub-chunks of the inbox in flight (64 B each per thread). The RS ring is a
+  // chain of tile epilogues across steps and each link pays these loads' latency: 4 in flight
+  // instead of 2 measured -2% on the per-GPU TP8 ring (8: no better, and spills).
+  constexpr int kD = kF32 ? 1 : kDepth;
   uint32_t r[32];
-  uint4 raw[2][kW];
+  uint4 raw[kD][kW];
   const bool pull = valid && inbox;
-  if (pull && kAhead) {
+  if (pull && kD > 1) {
 #pragma unroll
-    for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, 0, g, row));
+    for (int d = 0; d < kD; ++d)
+#pragma unroll
+      for (int g = 0; g < kW; ++g) raw[d][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, d, g, row));
   }
-#pragma unroll(kAhead ? kNJ : 1)
+#pragma unroll(kD > 1 ? kNJ : 1)
   for (int j = 0; j < kNJ; ++j) {
-    const int c = kAhead ? (j & 1) : 0;
-    if (pull) {
-      if (!kAhead) {
+    const int c = j % kD;
+    if (pull && kD == 1) {
 #pragma unroll
-        for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j, g, row));
-      } else if (j + 1 < kNJ) {
-#pragma unroll
-        for (int g = 0; g < kW; ++g)
-          raw[c ^ 1][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j + 1, g, row));
-      }
+      for (int g = 0; g < kW; ++g) raw[0][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j, g, row));
     }
     tmem_ld_32x32b_x32(taddr + j * 32, r);
     tmem_ld_wait();
@@ -474,6 +473,10 @@ __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t
           v[g * 8 + 4] = v[g * 8 + 4] + bf16lo(w.z); v[g * 8 + 5] = v[g * 8 + 5] + bf16hi(w.z);
           v[g * 8 + 6] = v[g * 8 + 6] + bf16lo(w.w); v[g * 8 + 7] = v[g * 8 + 7] + bf16hi(w.w);
         }
+      }
+      if (kD > 1 && j + kD < kNJ) {
+#pragma unroll
+        for (int g = 0; g < kW; ++g) raw[c][g] = *reinterpret_cast<const uint4*>(inbox + wire_off(kF32, j + kD, g, row));
       }
     }
     if (last)
@@ -1089,9 +1092,10 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         const uint32_t tempty_a = a ? tempty_leader1 : tempty_leader0;
         const int64_t ocol0 = static_cast<int64_t>(t.nt) * BN;
         if (p.wire_f32)
-          rs_epilogue_pipelined<true>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
+          rs_epilogue_pipelined<true, 1>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
         else
-          rs_epilogue_pipelined<false>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
+          rs_epilogue_pipelined<false, kMode == MODE_STD ? 4 : 2>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid,
+                                                                 last, tempty_a);
       }
       if (p.trace && lane == 0 && ew == 0 && tile_live)
         trace_rec(p, TR_EPI_LOOP, rank, t.step, lin, t_epi0, globaltimer());
