@@ -87,7 +87,6 @@ struct KParams {
   int group_m;         // raster: m-block pairs that sweep the n-tiles together
   int group_n;         // raster (when > 0, instead of group_m): n-tiles that the m-block pairs sweep
   int l2_a, l2_b;      // TMA L2 eviction priority of the A / B loads: 0 normal, 1 evict_first, 2 evict_last
-  int ag_nfwd;         // AG: leading n-tiles of an m-block that forward its images
   int ag_batch;        // AG: forwards per fence + flag publication (<= 16)
   int act;             // AG epilogue activation (Act)
   int a_mn;            // A operand MN-major (rows contiguous): x stored as (K_red, rows), e.g. X for X^T dY

@@ -525,8 +525,6 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint64_t* empty = bars + kSt;       // per CTA: 1 (leader's multicast commit)
   uint64_t* tfull = bars + 2 * kSt;   // per CTA: 1 (leader's multicast commit)
   uint64_t* tempty = bars + 2 * kSt + 2;  // leader: 8 epilogue warps of the pair
-  // per CTA, per forwarder group: a forwarded A stage landed (MMA -> forwarder)
-  uint64_t* fwd_ready = bars + 2 * kSt + 4;  // [2][kSt]
   uint64_t* fold_bar = bars + 4 * kSt + 4;   // [2 groups][2 buffers]: rs_direct fold staging
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kSt + 8);
   uint64_t* fwd_bar = bars + 4 * kSt + 9;    // [2]: A-carrying AG forwarder bulk loads
@@ -544,10 +542,8 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   const int per_step = p.npairs * p.nnt;
   const int ntiles = p.nsteps * per_step;
   const bool active = h < p.n_hosted;  // (grid is sized exactly; kept for safety)
-  // AG ring forwarding rides the A pipeline: the stage image is bulk-stored to the
-  // successor before the stage is recycled (so `empty` also waits for the forwarder).
+  // AG ring forwarding (warps 2-3, decoupled from the GEMM pipeline: see the forwarder branch)
   const bool fwd = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
-  const int nfwd = min(p.ag_nfwd, p.nnt);       // leading n-tiles that forward an m-block
   const int fbatch = min(max(p.ag_batch, 1), 8);  // forwards per fence + flag publication
 
   if (warp == 0 && lane == 0) {
@@ -561,9 +557,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kSt; ++s) {
       mbar_init(full + s, 2);
-      mbar_init(empty + s, (fwd && kGatherB) ? 2 : 1);
-      mbar_init(fwd_ready + s, 1);
-      mbar_init(fwd_ready + kSt + s, 1);
+      mbar_init(empty + s, 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull + a, 1);
@@ -637,8 +631,6 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
         int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
         uint64_t t_first = 0;
-        const int fwd_key = kGatherB ? t.pair : t.nt;  // which tiles forward (pair / n-tile)
-        const bool fwd_tile = fwd && it < p.T - 1 && fwd_key < nfwd;
         if (kMode == MODE_QSPLIT && t.valid > 0 && lane == 0 && !p.compute_only) {
           // the A rows of this step's query slice come from the concurrently running attention
           // kernel (generic stores): wait for the slice's counter, then order the TMA reads
@@ -696,9 +688,6 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
           }
           if (lane == 0) {
             mbar_wait(p, empty + stage, phase ^ 1);
-            // gather_b: stages the forwarder will not touch are arrived on its behalf (empty
-            // counts 2); the A-carrying AG forwards from global memory and never holds a stage.
-            if (kGatherB && fwd && !(fwd_tile && kb % nfwd == fwd_key)) mbar_arrive(empty + stage);
             uint8_t* sa = smem_a + stage * kAStageBytes;
             uint8_t* sb = smem_b + stage * kBStageBytes;
             const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
@@ -752,29 +741,15 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         int stage = 0;
         uint32_t phase = 0;
         int lt = 0;
-        int fo = 0;  // ordinal of forwarded stage uses (same sequence in all roles)
         for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
           const int a = lt & 1;
           const uint32_t use = static_cast<uint32_t>(lt >> 1);
           mbar_wait(p, tempty + a, (use & 1) ^ 1);
           tc_fence_after();
           const uint32_t d = tmem_base + a * BN;
-          int fwd_nt = -1;
-          if (fwd && kGatherB) {
-            const Tile t = get_tile(p, lin, 0);
-            const int it = t.step % p.T;
-            const int key = kGatherB ? t.pair : t.nt;
-            if (it < p.T - 1 && key < nfwd) fwd_nt = key;
-          }
           for (int kb = 0; kb < p.nkb; ++kb) {
             mbar_wait(p, full + stage, phase);
             tc_fence_after();
-            if (fwd_nt >= 0 && kb % nfwd == fwd_nt) {
-              uint64_t* fr = fwd_ready + ((fo / fbatch) & 1) * kSt + stage;
-              mbar_arrive(fr);
-              mbar_arrive_cluster(mapa_shared(smem_u32(fr), 1));
-              ++fo;
-            }
             const uint32_t abase = smem_u32(smem_a + stage * kAStageBytes);
             const uint32_t bbase = smem_u32(smem_b + stage * kBStageBytes);
   #pragma unroll
@@ -797,11 +772,12 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       }
     } else {
       // ===================================================== AG ring forwarders (warps 2-3)
-      if (fwd && !kGatherB) {
-        // A-carrying AG: the ring forward is decoupled from the GEMM. Every CTA's two
-        // forwarder warps take a share of each step's images (round-robin over all CTAs of
-        // the rank), step by step: step 0 copies from x (a tensor load puts the rows in the
-        // SW128 image layout, zero past K), step i > 0 copies the inbox image of slot i-1
+      if (fwd) {
+        // The ring forward is decoupled from the GEMM. Every CTA's two forwarder warps take a
+        // share of each step's images (round-robin over all CTAs of the rank), step by step:
+        // step 0 copies this rank's own operand (A: rows of x; gather_b: a 128-row half of a
+        // weight n-tile; a tensor load puts it in the SW128 image layout, zero past the
+        // edges), step i > 0 copies the inbox image of slot i-1
         // once the predecessor's flag is seen, into the successor's slot i. No pipeline
         // stage is ever held (gating stage reuse on a forwarder cost 10-18 us per call at
         // TP = 8), the work is spread over all SMs, and step i's sends depend only on the
@@ -833,7 +809,8 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
           if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
           nunpub = 0;
         };
-        const int nimg = p.nmb * p.nkb;
+        // images per slot: A rows per (m-block, k-block); gather_b B halves per (half, n-tile, k-block)
+        const int nimg = kGatherB ? 2 * p.nnt * p.nkb : p.nmb * p.nkb;
         for (int pass = 0; pass < p.m; ++pass) {
           for (int it = 0; it < p.T - 1; ++it) {
             const int slot = pass * (p.T - 1) + it;
@@ -841,10 +818,10 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             cur_dst = p.sched[rank][it][0];
             const uint64_t t0 = p.trace ? globaltimer() : 0;
             for (int img = fw; img < nimg; img += nfw) {
-              const int mb = img / p.nkb, kb = img - mb * p.nkb;
+              const int mb = img / p.nkb, kb = img - mb * p.nkb;  // gather_b: mb = half * nnt + n-tile
               const int bb = mb / p.nmb_per_batch, j = mb - bb * p.nmb_per_batch;
               const int row0 = j * BM;
-              if (p.Sc - row0 <= 0) continue;  // padding m-block of an odd pair: never read
+              if (!kGatherB && p.Sc - row0 <= 0) continue;  // padding m-block of an odd pair: never read
               if (lane == 0) {
                 char* dst = slot_ptr(p, par, cur_dst, slot) + static_cast<int64_t>(img) * kAStageBytes;
                 bulk_wait_read<0>();  // the previous store has read the buffer
@@ -852,7 +829,10 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
                   // rows past this chunk are read as whatever x holds there (their products
                   // are never stored)
                   mbar_arrive_expect_tx(fbar, kAStageBytes);
-                  tma_load_4d(fbuf, &p.tmap_a, fbar, kb * BK, pass * static_cast<int>(p.Sc) + row0, bb, h);
+                  if (kGatherB)  // K-major B: 64 K x 128 N box of half mb / nnt of n-tile mb % nnt
+                    tma_load_3d(fbuf, &p.tmap_b, fbar, kb * BK, (mb % p.nnt) * BN + (mb / p.nnt) * (BN / 2), h);
+                  else
+                    tma_load_4d(fbuf, &p.tmap_a, fbar, kb * BK, pass * static_cast<int>(p.Sc) + row0, bb, h);
                 } else {
                   const uint32_t* fsrc = flag_ptr(p, par, rank, slot - 1, img);
                   wait_flag(p, fsrc, rank, p.sched[rank][it - 1][1], pass * p.T + it, img, ep);
@@ -872,72 +852,6 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             if (nunpub > 0) flush();
             if (p.trace && lane == 0) trace_rec(p, TR_AG_PIECE, rank, slot, fw, t0, globaltimer());
           }
-        }
-      } else if (fwd) {
-        // DP parameter all-gather (gather_b: the ring carries weight row blocks): forwarded
-        // stage uses (tile pair < nfwd, k-block kb % nfwd == pair) are split into batches of
-        // fbatch alternating between the two warps. For each of its uses a warp waits on its
-        // fwd_ready barrier, copies the landed 16 KiB SWIZZLE_128B image out of SMEM
-        // (ld.shared, synchronous -> the stage is released at once) and posts st.global.v4
-        // into the successor's slot. At the end of its batch (and of every tile) the warp
-        // fences its stores at system scope and publishes the image flags. Flags never stay
-        // unpublished across a tile boundary (step-i images depend only on step i-1).
-        const int grp = warp - 2;
-        uint32_t* unpub[16];
-        int nunpub = 0;
-        uint32_t ph = 0;  // per-stage phase bits of this group's fwd_ready barriers
-        int fo = 0;
-        auto flush = [&]() {
-          const uint64_t tf0 = p.trace ? globaltimer() : 0;
-          fence_sys();
-          __syncwarp();
-          if (lane == 0 && rank != p.fault_rank)
-            for (int i = 0; i < nunpub; ++i) st_relaxed_sys(unpub[i], ep);
-          if (p.trace && lane == 0) trace_rec(p, TR_FLUSH, rank, 0, nunpub, tf0, globaltimer());
-          nunpub = 0;
-        };
-        int lt = 0;
-        for (int lin = gp; lin < ntiles; lin += GP, ++lt) {
-          const Tile t = get_tile(p, lin, cta);
-          const int pass = t.step / p.T, it = t.step - pass * p.T;
-          const int key = kGatherB ? t.pair : t.nt;
-          if (!(it < p.T - 1 && key < nfwd)) continue;
-          const int slot = pass * (p.T - 1) + it;
-          const int dst_rank = p.sched[rank][it][0];
-          const uint64_t t0 = p.trace ? globaltimer() : 0;
-          // forwarded operand: this CTA's A rows, or (gather_b) its half of the B tile
-          const bool live = kGatherB ? true : t.valid > 0;
-          const int64_t img0 = kGatherB ? (static_cast<int64_t>(cta) * p.nnt + t.nt) * p.nkb
-                                          : static_cast<int64_t>(t.mb) * p.nkb;
-          const uint8_t* sbase = kGatherB ? smem_b : smem_a;
-          for (int kb = key; kb < p.nkb; kb += nfwd) {
-            const bool mine = ((fo / fbatch) & 1) == grp;
-            const bool batch_end = (fo % fbatch) == fbatch - 1;
-            ++fo;
-            if (!mine) continue;
-            const int stage = static_cast<int>((static_cast<int64_t>(lt) * p.nkb + kb) % kSt);
-            mbar_wait(p, fwd_ready + grp * kSt + stage, (ph >> stage) & 1u);
-            ph ^= 1u << stage;
-            if (live) {
-              const int64_t img = img0 + kb;
-              const uint4* src = reinterpret_cast<const uint4*>(sbase + stage * kAStageBytes);
-              uint4* dst = reinterpret_cast<uint4*>(slot_ptr(p, par, dst_rank, slot) + img * kAStageBytes);
-  #pragma unroll
-              for (int half = 0; half < 2; ++half) {
-                uint4 v[16];
-  #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = src[(half * 16 + i) * 32 + lane];
-  #pragma unroll
-                for (int i = 0; i < 16; ++i) dst[(half * 16 + i) * 32 + lane] = v[i];
-              }
-              unpub[nunpub++] = flag_ptr(p, par, dst_rank, slot, img);
-            }
-            __syncwarp();  // every lane's SMEM reads of the stage are done
-            if (lane == 0) mbar_arrive(empty + stage);
-            if (batch_end && nunpub > 0) flush();
-          }
-          if (nunpub > 0) flush();
-          if (p.trace && lane == 0 && live) trace_rec(p, TR_AG_PIECE, rank, slot, lin, t0, globaltimer());
         }
       }
     }
@@ -1185,7 +1099,7 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
   static uint64_t attr_done = 0;
   static bool pool_ok[64];
   constexpr int kSmem = kMode == MODE_RS_DIRECT                        ? kSmemBytesDirect
-                        : (kOp == OP_AG && kMode == MODE_STD) ? kSmemBytesFwd
+                        : (kOp == OP_AG && (kMode == MODE_STD || kMode == MODE_GATHER_B)) ? kSmemBytesFwd
                                                               : kSmemBytes;
   once_per_device(attr_done, [kern] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);

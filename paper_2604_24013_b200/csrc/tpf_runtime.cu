@@ -388,7 +388,6 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   if (const char* e = std::getenv("TPF_GROUP_N")) p.group_n = std::atoi(e);  // dev A/B overrides
   if (const char* e = std::getenv("TPF_L2_A")) p.l2_a = std::atoi(e);
   if (const char* e = std::getenv("TPF_L2_B")) p.l2_b = std::atoi(e);
-  p.ag_nfwd = env_int("TPF_AG_NFWD", 4);
   p.ag_batch = env_int("TPF_AG_BATCH", 4);
   p.nsteps = k.T * k.m;
   p.B = static_cast<int>(k.B);

@@ -46,6 +46,20 @@ for cfg, S, K_ag, N_ag, K_rs, N_rs in (("cfg2", 8192, 4096, 28672, 14336, 4096),
     res[cfg + "_ag_co"] = loop(lambda: comm.ag_gemm(x, w, y))
     comm.set_compute_only(False)
     comm.close()
+if T == 8:
+    # cfg4 DP per GPU: parameter AG fused into the forward GEMM (gather_b) and gradient RS
+    M, K, N = 4096, 2048, 8192
+    g = torch.Generator(device=dev).manual_seed(1)
+    X = torch.randn((M, K), device=dev, generator=g).to(torch.bfloat16)
+    dY = (torch.randn((M, N), device=dev, generator=g) / 64).to(torch.bfloat16)
+    dW = torch.empty((K // T, N), device=dev, dtype=torch.bfloat16)
+    Wr = (torch.randn((N // T, K), device=dev, generator=g) / 45).to(torch.bfloat16)
+    out = torch.empty((M, N), device=dev, dtype=torch.bfloat16)
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_rs(T, 1, K, M, N, 1, tpf.BF16),
+                                                 tpf.sym_bytes_dp_ag(T, K, N // T)))
+    res["cfg4_param_ag"] = loop(lambda: comm.dp_param_ag_gemm(X, Wr, out))
+    res["cfg4_grad_rs"] = loop(lambda: comm.dp_grad_rs(X, dY, dW, kind=tpf.RING, wire=tpf.BF16))
+    comm.close()
 print(json.dumps(res))
 '''
 libs = sys.argv[1:3]

@@ -59,24 +59,10 @@ if pieces:
               f"mean piece {d / n / 1e3:6.2f} us  n={n}")
 print("no_tail:", trace.no_tail(summ))
 
-# main-loop durations by (forwarding tile?) -- reproduce the kernel's pair-tile raster
+# main-loop durations (every AG tile reads its operand the same way: forwarding is decoupled)
 if op == "ag":
-    per_step_pairs = ((S // T + 127) // 128 + 1) // 2
-    nnt = (2 * F // T + 255) // 256
-    GM = int(os.environ.get("TPF_GROUP_M", "16"))
-    nfwd = min(int(os.environ.get("TPF_AG_NFWD", "4")), nnt)
-
-    def nt_of(lin):
-        rem = lin % (per_step_pairs * nnt)
-        g0 = (rem // (GM * nnt)) * GM
-        gm = min(GM, per_step_pairs - g0)
-        return (rem - g0 * nnt) // gm
-
-    ml = [rr for rr in recs if rr.kind == trace.TR_MAINLOOP and rr.rank == 0]
-    fw = [(rr.t1 - rr.t0) / 1e3 for rr in ml if nt_of(rr.index) < nfwd and rr.step < T - 1]
-    nf = [(rr.t1 - rr.t0) / 1e3 for rr in ml if not (nt_of(rr.index) < nfwd and rr.step < T - 1)]
-    print(f"rank0 mainloop(us): forwarding tiles n={len(fw)} mean={sum(fw) / max(1, len(fw)):.1f}  "
-          f"others n={len(nf)} mean={sum(nf) / max(1, len(nf)):.1f}")
+    ml = [(rr.t1 - rr.t0) / 1e3 for rr in recs if rr.kind == trace.TR_MAINLOOP and rr.rank == 0]
+    print(f"rank0 mainloop(us): n={len(ml)} mean={sum(ml) / max(1, len(ml)):.1f}")
     ep = [(rr.t1 - rr.t0) / 1e3 for rr in recs if rr.kind == trace.TR_TILE and rr.rank == 0]
     print(f"rank0 epilogue(us): mean={sum(ep) / max(1, len(ep)):.1f} max={max(ep):.1f}")
     fl = [rr for rr in recs if rr.kind == 7 and rr.rank == 0]
