@@ -1,5 +1,6 @@
 """Dev tool: A/B library builds (TPF_LIB_PATH) on the UP attention (cfg5 T = 8 local group and a
-per-GPU shape), alternating fresh processes.   python tools/ab_up.py LIB_A LIB_B ... [--rounds N]"""
+per-GPU shape), alternating fresh processes.   python tools/ab_up.py LIB_A LIB_B ... [--rounds N]
+A spec may carry environment settings: 'lib.so@TPF_FMHA_PAIR=0'."""
 import os
 import statistics
 import subprocess
@@ -33,7 +34,9 @@ args = [a for a in args if not a.isdigit()]
 res = {a: [] for a in args}
 for _ in range(rounds):
     for lib in args:
-        env = dict(os.environ, TPF_LIB_PATH=os.path.abspath(lib))
+        path, *kvs = lib.split("@")  # 'lib.so@ENV=V' runs the build under an environment setting
+        env = dict(os.environ, TPF_LIB_PATH=os.path.abspath(path))
+        env.update(kv.split("=", 1) for kv in kvs)
         r = subprocess.run([sys.executable, "-c", CODE], env=env, capture_output=True, text=True, timeout=900)
         try:
             res[lib].append([float(x) for x in r.stdout.strip().splitlines()[-1].split()])
