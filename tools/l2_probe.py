@@ -12,6 +12,16 @@ import paper_2604_24013_b200 as tpf
 
 op = sys.argv[1]
 dev = torch.device("cuda:0")
+if os.environ.get("PERSIST_MB"):
+    # L2 set-aside for persisting (evict_last) lines, cudaLimitPersistingL2CacheSize = 0x06
+    import ctypes
+    torch.cuda.init()
+    rt = ctypes.CDLL("libcudart.so.12")
+    mx = ctypes.c_int(0)
+    rt.cudaDeviceGetAttribute(ctypes.byref(mx), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+    want = min(int(os.environ["PERSIST_MB"]) << 20, mx.value)
+    print("persisting L2 set-aside", want >> 20, "MB of max", mx.value >> 20, "MB; rc",
+          rt.cudaDeviceSetLimit(6, ctypes.c_size_t(want)))
 g = torch.Generator(device=dev).manual_seed(0)
 one = tpf.Communicator.create(0, 1, 0)
 if op == "rs":
