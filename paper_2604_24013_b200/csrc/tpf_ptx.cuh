@@ -271,6 +271,9 @@ __device__ __forceinline__ void group_abort_store(uint32_t* const* tables, int T
 // waiter that gives up on a peer flag; awaited == waiter marks a rank that failed itself.
 __device__ __forceinline__ void blame_store(uint32_t* const* tables, int T, int waiter, int awaited) {
   if (!tables[0] || waiter < 0 || awaited < 0) return;
+  // A rank that marked itself failed keeps the mark: if it later gives up on a peer itself (the
+  // group abort reaches it mid-wait), overwriting the mark would turn the chain into a cycle.
+  if (awaited != waiter && ld_relaxed_sys(tables[waiter] + waiter) == static_cast<uint32_t>(waiter + 1)) return;
   for (int x = 0; x < T; ++x) st_relaxed_sys(tables[x] + waiter, static_cast<uint32_t>(awaited + 1));
   fence_sys();
 }

@@ -825,6 +825,10 @@ int tpf_comm_sync(tpf_comm* c, void* stream) {
         if (a == r || a < 0 || a >= c->world) break;
         r = a;
       }
+      // A rank that marked itself failed is the failing rank, whatever the waiters' links say
+      // (they are recorded as each waiter gives up, and a late give-up can leave a gap).
+      for (int x = 0; x < c->world; ++x)
+        if (tab[x] == static_cast<uint32_t>(x + 1)) r = x;
       culprit = r;
       const int nheaps = c->local_group ? c->world : 1;
       for (int h = 0; h < nheaps; ++h)
