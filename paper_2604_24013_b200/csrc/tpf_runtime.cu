@@ -814,13 +814,13 @@ int tpf_comm_sync(tpf_comm* c, void* stream) {
     // record their give-ups within microseconds of ours; a short grace covers the race.
     int culprit = waiter;
     uint32_t tab[tpf::kMaxRanks] = {};
-    const bool have_tables = c->world > 1 && !c->is_virtual && waiter >= 0 && waiter < c->world;
+    const bool have_tables = c->world > 1 && !c->is_virtual;
     if (have_tables) {
       std::this_thread::sleep_for(std::chrono::milliseconds(20));
       char* own = c->local_group ? c->local : c->sym[c->rank];
       TPF_CUDA_TRY(cudaMemcpy(tab, own + kBlameOff, sizeof(tab), cudaMemcpyDeviceToHost));
-      int r = waiter;
-      for (int n = 0; n <= c->world && tab[r] != 0; ++n) {
+      int r = waiter;  // -1: a pipeline-barrier timeout, no waiter to start the chain from
+      for (int n = 0; r >= 0 && r < c->world && n <= c->world && tab[r] != 0; ++n) {
         const int a = static_cast<int>(tab[r]) - 1;
         if (a == r || a < 0 || a >= c->world) break;
         r = a;
