@@ -29,7 +29,7 @@ constexpr int kFoldUnit = BM * 16;                                  // 2 KiB
 constexpr int kFoldGroupBytes = 2 * (kMaxRanks - 1) * kFoldUnit;    // 28 KiB per warpgroup
 constexpr int kSmemBytesDirect = kStagesDirect * kStageBytes + 2048 + 2 * kFoldGroupBytes + 1024;
 static_assert(kSmemBytesDirect <= 227 * 1024, "pairwise instance exceeds the shared-memory limit");
-// A-carrying AG-GEMM (MODE_STD): two 16 KiB forwarder bounce buffers after 1 KiB of barriers
+// AG-GEMM instances (MODE_STD, MODE_GATHER_B): two 16 KiB forwarder bounce buffers after 1 KiB of barriers
 // (+ 1 KiB alignment slack; the kernel's 1 KiB of static shared memory counts against 227 KiB)
 constexpr int kSmemBytesFwd = kStages * kStageBytes + 1024 + 2 * kAStageBytes + 1024;
 static_assert(kSmemBytesFwd + 1024 <= 227 * 1024, "AG instance exceeds the shared-memory limit");
@@ -87,7 +87,7 @@ struct KParams {
   int group_m;         // raster: m-block pairs that sweep the n-tiles together
   int group_n;         // raster (when > 0, instead of group_m): n-tiles that the m-block pairs sweep
   int l2_a, l2_b;      // TMA L2 eviction priority of the A / B loads: 0 normal, 1 evict_first, 2 evict_last
-  int ag_batch;        // AG: forwards per fence + flag publication (<= 16)
+  int ag_batch;        // AG: forwarded images per fence + flag publication (clamped to 1..8)
   int act;             // AG epilogue activation (Act)
   int a_mn;            // A operand MN-major (rows contiguous): x stored as (K_red, rows), e.g. X for X^T dY
   int b_kmajor;        // B operand K-major: w stored (N, K) row-major (PyTorch Linear weight layout)

@@ -527,9 +527,9 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint64_t* tempty = bars + 2 * kSt + 2;  // leader: 8 epilogue warps of the pair
   uint64_t* fold_bar = bars + 4 * kSt + 4;   // [2 groups][2 buffers]: rs_direct fold staging
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kSt + 8);
-  uint64_t* fwd_bar = bars + 4 * kSt + 9;    // [2]: A-carrying AG forwarder bulk loads
+  uint64_t* fwd_bar = bars + 4 * kSt + 9;    // [2]: AG forwarder warps, their bulk / tensor loads
   uint8_t* fold_smem = smem + kSt * kStageBytes + 2048;  // MODE_RS_DIRECT: [2 groups][kFoldGroupBytes]
-  uint8_t* fwd_smem = smem + kSt * kStageBytes + 1024;   // A-carrying AG: 2 x 16 KiB forwarder buffers
+  uint8_t* fwd_smem = smem + kSt * kStageBytes + 1024;   // AG (both kinds): 2 x 16 KiB forwarder buffers
 
   // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
