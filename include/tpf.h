@@ -92,12 +92,13 @@ int tpf_comm_open_peers(tpf_comm* c, const void* handles /* world * TPF_IPC_HAND
  * out[world][...]. */
 int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm** out);
 
-/* Performance-only: rank 0 of a `world`-rank group whose peers are virtual: their heaps
+/* Measurement tool: rank 0 of a `world`-rank group whose peers are virtual: their heaps
  * alias this rank's own heap (a self-ring), so each send fills the slot this rank reads one
- * step later and the ring's step-to-step waits are real, with zero link latency (the flags
- * start pre-set, so the first call after creation does not wait). Runs the full per-rank
- * protocol at full-GPU scale -- what one GPU of a TP group computes -- but the results are
- * meaningless. For measurement tools only. */
+ * step later and the ring's step-to-step waits are real from the first call, with zero link
+ * latency. Runs the full per-rank protocol at full-GPU scale -- what one GPU of a TP group
+ * computes. The results are well defined but are not a real group's: the AG gathers the own
+ * slice at every step; the GEMM-RS sums the GEMMs of every row slice; the all-to-all
+ * attention paths have no other sources and skip their receive waits. */
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out);
 /* Split group: `world` communicators on the current GPU, one per rank, each with its own
  * symmetric heap, device epoch and error record -- tpf_comm_create's per-process

@@ -272,10 +272,12 @@ class Communicator:
 
     @classmethod
     def virtual_group(cls, world: int, sym_bytes: int) -> "Communicator":
-        """Performance-only: rank 0 of a `world`-rank group with virtual peers. The peers alias
+        """Measurement tool: rank 0 of a `world`-rank group with virtual peers. The peers alias
         this rank's own heap (a self-ring): each send fills the slot this rank reads one step
         later, so the ring's step-to-step waits are real (zero link latency). Per-rank
-        tensors, full-GPU scale; results are meaningless. See tpf_comm_create_virtual."""
+        tensors, full-GPU scale. Results are well defined but not a real group's (the AG
+        gathers the own slice every step, the GEMM-RS sums every row slice's GEMM;
+        tests/test_gpu_virtual.py). See tpf_comm_create_virtual."""
         h = C.c_void_p()
         _check(_lib.tpf_comm_create_virtual(world, sym_bytes, C.byref(h)))
         return cls(h.value, 0, world, False)

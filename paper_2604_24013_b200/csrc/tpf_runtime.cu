@@ -671,25 +671,19 @@ int tpf_comm_create_local_group(int world, size_t sym_bytes_per_rank, tpf_comm**
 }
 
 int tpf_comm_create_virtual(int world, size_t sym_bytes, tpf_comm** out) {
-  // Performance-only: rank 0 of a `world`-rank group on this GPU, with every peer virtual.
+  // Measurement tool: rank 0 of a `world`-rank group on this GPU, with every peer virtual.
   // Peer heaps alias this rank's own heap (a self-ring), so a send lands in this rank's inbox
   // slot of the same index -- the slot the real successor would fill -- and is read one step
-  // later while still L2-resident, as data arriving over NVLink would be. The flag blocks start
-  // pre-set to 0xFFFFFFFF only so that the FIRST call after creation does not wait on flags
-  // nobody writes; every send overwrites its flag with the call's epoch, so from the second
-  // call on each step's wait is real: it passes when this rank's own previous-step send lands.
-  // The kernels run the real protocol instructions at full-GPU scale, which measures what one
-  // GPU of a TP group computes. Results are NOT meaningful.
+  // later while still L2-resident, as data arriving over NVLink would be. Every flag a step
+  // waits on is written by this rank's own previous-step send in the same call, so every
+  // wait is real from the first call on (flags start at zero like any communicator's). The
+  // kernels run the real protocol instructions at full-GPU scale, which measures what one GPU
+  // of a TP group computes; the results are well defined (tests/test_gpu_virtual.py): the AG
+  // gathers the own slice at every step, the GEMM-RS sums the GEMMs of every row slice.
   tpf_comm* c = nullptr;
   int rc = tpf_comm_create(0, world, sym_bytes, &c);
   if (rc != TPF_OK) return rc;
   c->is_virtual = 1;
-  cudaError_t e = cudaMemset(c->local, 0xFF, kBlameOff);  // every flag pre-set; blame table stays zero
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    tpf_comm_destroy(c);
-    return fail(tpf::Status::cuda(std::string("tpf_comm_create_virtual: ") + cudaGetErrorString(e)));
-  }
   for (int r = 1; r < world; ++r) c->sym[r] = c->local;
   c->peers_ready = true;
   *out = c;
@@ -1002,11 +996,13 @@ static tpf::Status fmha_a2a_v2(tpf_comm* c, const void* const qkv[3], const void
     const int rank = r0 + hh;
     uint32_t* f0 = flags_at(rank, 0);
     uint32_t* f1 = flags_at(rank, 1);
-    tpf::launch_wait_flags2(f0, f1, static_cast<int64_t>(rank) * nflags2, c->dev_epoch, 0, c->timeout_ns, c->err,
-                            rank, blame_of(c), 0, nflags2, stream);
-    const int64_t off = static_cast<int64_t>(rank + 1) * nflags2;
-    tpf::launch_wait_flags2(f0 + off, f1 + off, static_cast<int64_t>(T - 1 - rank) * nflags2, c->dev_epoch, 0,
-                            c->timeout_ns, c->err, rank, blame_of(c), off, nflags2, stream);
+    if (!c->is_virtual) {  // virtual group: the only source is this rank (self-ring), nothing comes in
+      tpf::launch_wait_flags2(f0, f1, static_cast<int64_t>(rank) * nflags2, c->dev_epoch, 0, c->timeout_ns, c->err,
+                              rank, blame_of(c), 0, nflags2, stream);
+      const int64_t off = static_cast<int64_t>(rank + 1) * nflags2;
+      tpf::launch_wait_flags2(f0 + off, f1 + off, static_cast<int64_t>(T - 1 - rank) * nflags2, c->dev_epoch, 0,
+                              c->timeout_ns, c->err, rank, blame_of(c), off, nflags2, stream);
+    }
     tpf::launch_copy_by_parity(static_cast<char*>(out) + hh * recv_bytes, recv_at(rank, 0), recv_at(rank, 1),
                                recv_bytes, c->dev_epoch, stream);
   }
@@ -1105,11 +1101,13 @@ int tpf_attention_a2a(tpf_comm* c, const void* q, const void* k, const void* v, 
   for (int h = 0; h < R; ++h) {
     const int rank = r0 + h;
     uint32_t* f = flags_of(rank);
-    tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags, epoch, c->timeout_ns, c->err, rank, blame_of(c), 0,
-                           nflags, stream);
-    tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags, static_cast<int64_t>(T - 1 - rank) * nflags,
-                           epoch, c->timeout_ns, c->err, rank, blame_of(c), static_cast<int64_t>(rank + 1) * nflags,
-                           nflags, stream);
+    if (!c->is_virtual) {  // virtual group: the only source is this rank (self-ring), nothing comes in
+      tpf::launch_wait_flags(f, static_cast<int64_t>(rank) * nflags, epoch, c->timeout_ns, c->err, rank, blame_of(c),
+                             0, nflags, stream);
+      tpf::launch_wait_flags(f + static_cast<int64_t>(rank + 1) * nflags, static_cast<int64_t>(T - 1 - rank) * nflags,
+                             epoch, c->timeout_ns, c->err, rank, blame_of(c), static_cast<int64_t>(rank + 1) * nflags,
+                             nflags, stream);
+    }
     TPF_CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(out) + h * recv_bytes, recv_of(rank), recv_bytes,
                                  cudaMemcpyDeviceToDevice, stream));
   }
@@ -1365,8 +1363,8 @@ static tpf::Status ulysses_first_a2a(tpf_comm* c, const void* q, const void* k, 
   up.fault_rank = c->fault_rank;
   tpf::launch_ulysses_push(up, stream);
   TPF_CUDA_TRY_STATUS(cudaGetLastError());
-  for (int hh = 0; hh < R; ++hh) {
-    const int rank = r0 + hh;
+  for (int hh = 0; hh < R && !c->is_virtual; ++hh) {  // virtual group: no other sources (the own part is
+    const int rank = r0 + hh;                          // stream-ordered after the push)
     tpf::launch_wait_flags2(up.flags[0][rank], up.flags[1][rank], static_cast<int64_t>(T) * up.ctas_per_rank,
                             c->dev_epoch, 0, c->timeout_ns, c->err, rank, blame_of(c), 0, up.ctas_per_rank, stream);
   }

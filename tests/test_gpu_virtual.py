@@ -1,0 +1,56 @@
+"""The per-GPU virtual group (Communicator.virtual_group: one rank of a T-rank group at full-GPU
+scale, every peer aliasing the rank's own heap, i.e. a self-ring) computes well-defined results,
+so the per-GPU measurements run the protocol on correct data paths. On integer data (exact in
+bf16 / fp32) at the BASELINE per-rank shapes:
+  * AG-GEMM: every step gathers the rank's own slice, so every row block of the output is x @ w;
+  * GEMM-RS (ring, fp32 wire): step i adds the GEMM of row slice l_i (ring_indices_rs) to the
+    running sum it received from itself, so the output is the sum over all row slices of
+    x[slice] @ w (the schedule visits every slice once).
+"""
+import pytest
+import torch
+
+import paper_2604_24013_b200 as tpf
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+
+
+def _ints(shape, lo, hi, seed):
+    g = torch.Generator(device=DEV).manual_seed(seed)
+    return torch.randint(lo, hi, shape, device=DEV, generator=g, dtype=torch.int32)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
+def test_virtual_tp8_ag_gemm_exact(cfg):
+    T = 8
+    S, K, N = {"cfg2": (8192, 4096, 28672), "cfg3": (16384, 8192, 10240)}[cfg]
+    sl, nl = S // T, N // T
+    x = _ints((1, sl, K), 0, 5, 1)
+    w = _ints((K, nl), -2, 2, 2)
+    want = (x[0].double() @ w.double()).float()
+    comm = tpf.Communicator.virtual_group(T, tpf.sym_bytes_ag(T, 1, S, K, nl))
+    for _ in range(3):  # both heap parities, and again
+        out = torch.full((1, S, nl), float("nan"), device=DEV)
+        comm.ag_gemm(x.to(torch.bfloat16), w.to(torch.bfloat16), out)
+        comm.sync()
+        for r in range(T):
+            assert torch.equal(out[0, r * sl:(r + 1) * sl], want), r
+    comm.close()
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
+def test_virtual_tp8_gemm_rs_ring_exact(cfg):
+    T = 8
+    S, K, N = {"cfg2": (8192, 14336, 4096), "cfg3": (16384, 8192, 8192)}[cfg]
+    kl, sl = K // T, S // T
+    x = _ints((1, S, kl), 0, 5, 3)
+    w = _ints((kl, N), -2, 2, 4)
+    want = (x[0].double() @ w.double()).view(T, sl, N).sum(0).float()  # |sum| < 2^24: exact
+    comm = tpf.Communicator.virtual_group(T, tpf.sym_bytes_rs(T, 1, S, kl, N, 1, tpf.F32))
+    for _ in range(3):
+        out = torch.full((1, sl, N), float("nan"), device=DEV)
+        comm.gemm_rs(x.to(torch.bfloat16), w.to(torch.bfloat16), out, kind=tpf.RING, wire=tpf.F32)
+        comm.sync()
+        assert torch.equal(out[0], want)
+    comm.close()

@@ -22,9 +22,9 @@ wr = (torch.randn((F // T, D), device=dev, generator=g) / 64).to(torch.bfloat16)
 yr = torch.empty((1, S // T, D), device=dev, dtype=torch.bfloat16)
 comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, D, 2 * F // T),
                                              tpf.sym_bytes_rs(T, 1, S, F // T, D, 1, tpf.BF16)))
-# four calls of each: profile the last pair (ncu -s 6 -c 2). Replays restore memory to the state
-# before the profiled launch, where the flags hold the previous call's epoch, so the ring's
-# step-to-step waits are real in the capture (a first call would pass the pre-set flags at once).
+# four calls of each: profile the last pair (ncu -s 6 -c 2), at steady state. Replays restore
+# memory to the state before the profiled launch, so the ring's step-to-step waits are real in
+# the capture.
 for _ in range(4):
     comm.ag_gemm(x, w, y)
     comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.BF16)
