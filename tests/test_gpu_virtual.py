@@ -54,3 +54,31 @@ def test_virtual_tp8_gemm_rs_ring_exact(cfg):
         comm.sync()
         assert torch.equal(out[0], want)
     comm.close()
+
+
+def test_virtual_dp_grad_rs_and_param_ag_exact():
+    """cfg 4 per-GPU shapes (8 ranks, 4096 tokens / rank, 2048 x 8192 weight): the gradient RS
+    sums the own X^T dY over every row slice of dW; the parameter AG gathers the own weight
+    block at every step, so every column block of the output is X . W_own^T."""
+    T, M, K, N = 8, 4096, 2048, 8192
+    X = _ints((M, K), 0, 5, 5)
+    dY = _ints((M, N), -2, 2, 6)
+    kl = K // T
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_rs(T, 1, K, M, N, 1, tpf.F32),
+                                                 tpf.sym_bytes_dp_ag(T, K, N // T)))
+    want = (X.double().t() @ dY.double()).view(T, kl, N).sum(0).float()  # < 2^24: exact
+    dW = torch.full((kl, N), float("nan"), device=DEV)
+    for _ in range(2):
+        comm.dp_grad_rs(X.to(torch.bfloat16), dY.to(torch.bfloat16), dW, kind=tpf.RING, wire=tpf.F32)
+        comm.sync()
+        assert torch.equal(dW, want)
+    Nl = N // T
+    Wr = _ints((Nl, K), -2, 2, 7)
+    blk = (X.double() @ Wr.double().t()).float()
+    out = torch.full((M, N), float("nan"), device=DEV)
+    for _ in range(2):
+        comm.dp_param_ag_gemm(X.to(torch.bfloat16), Wr.to(torch.bfloat16), out)
+        comm.sync()
+        for j in range(T):
+            assert torch.equal(out[:, j * Nl:(j + 1) * Nl], blk), j
+    comm.close()
