@@ -193,3 +193,18 @@ def test_query_split_attention_T8_vs_oracle(kind):
     comm.close()
     want = O.query_split_attention(T, kind, batch, heads, q, k, v, w_o)
     assert rel_deviation(out.double().cpu().numpy(), want) <= 2e-2
+
+
+@pytest.mark.parametrize("M,K,N", [(8192, 4096, 28672), (8192, 14336, 4096), (4096, 4096, 4864), (2048, 8192, 1280)],
+                         ids=["bench_up_wide", "bench_down_narrow", "narrow_partial_group", "cfg3_qkv_per_rank"])
+def test_fullsize_t1_gemm_exact(M, K, N):
+    """The T = 1 GEMM (MODE_SINGLE) at the bench block's shapes and through the raster paths its
+    heuristics pick (tpf_runtime.cu: wide N -> evict_last A panels; narrow N -> group_n n-tile
+    sweeps with an evict_last B slab, including a last group of fewer n-tiles): exact integer
+    product in fp32 (|sums| < 2^24)."""
+    x = _ints((M, K), 0, 5, 11)
+    w = _ints((K, N), -2, 2, 12)
+    out = torch.full((M, N), float("nan"), device=DEV)
+    tpf.gemm(x.to(torch.bfloat16), w.to(torch.bfloat16), out)
+    torch.cuda.synchronize()
+    assert torch.equal(out.double(), x.double() @ w.double())
