@@ -208,3 +208,25 @@ def test_fullsize_t1_gemm_exact(M, K, N):
     tpf.gemm(x.to(torch.bfloat16), w.to(torch.bfloat16), out)
     torch.cuda.synchronize()
     assert torch.equal(out.double(), x.double() @ w.double())
+
+
+def test_fullsize_t1_swiglu_bench_shape():
+    """The bench block's first GEMM as the bench runs it: T = 1, 8192 x 4096 x (2 x 14336) with
+    SwiGLU fused in the epilogue over the tile-interleaved gate||up weight, bf16 output, against
+    an fp32 torch reference (bf16 output rounding: 1e-2 of the max)."""
+    S, D, F = 8192, 4096, 14336
+    g = torch.Generator(device=DEV).manual_seed(21)
+    x = torch.randn((1, S, D), device=DEV, generator=g).to(torch.bfloat16)
+    gate = (torch.randn((D, F), device=DEV, generator=g) / D ** 0.5).to(torch.bfloat16)
+    up = (torch.randn((D, F), device=DEV, generator=g) / D ** 0.5).to(torch.bfloat16)
+    w = tpf.interleave_gate_up(gate, up).contiguous()
+    out = torch.empty((1, S, F), device=DEV, dtype=torch.bfloat16)
+    one = tpf.Communicator.create(0, 1, 0)
+    one.ag_gemm(x, w, out, act=tpf.ACT_SWIGLU)
+    one.sync()
+    one.close()
+    xf = x[0].float()
+    for c0 in (0, F // 2, F - 2048):  # three column bands keep the fp32 reference small
+        ref = torch.nn.functional.silu(xf @ gate[:, c0:c0 + 2048].float()) * (xf @ up[:, c0:c0 + 2048].float())
+        err = (out[0, :, c0:c0 + 2048].float() - ref).abs().max().item()
+        assert err <= 1e-2 * ref.abs().max().item(), (c0, err)
