@@ -208,6 +208,48 @@ def traced_tail(comm, fn, dev):
     return max((v["tail_us"] for v in summ.values()), default=0.0)
 
 
+
+def e2e_pipeline(torch, n, x_host, y_host, x_dev, y_dev, compute, stream, dev, barrier=lambda: None):
+    """The e2e timed region: n steps, each copying its input from pinned host memory
+    (x_host[i % nbuf] -> x_dev) on one stream, running compute(x_dev[b], y_dev[b]) on the
+    compute stream and copying the result back (y_dev[b] -> y_host[b]) on another, with
+    nbuf-deep double buffering so step i+1's H2D and step i-1's D2H overlap step i's kernels.
+    Returns ms per step (first H2D start to last D2H end). Tested for correct ordering in
+    tests/test_gpu_e2e.py."""
+    nbuf = len(x_host)
+    s_in = torch.cuda.Stream(dev)
+    s_out = torch.cuda.Stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(n)]
+    ev_done = [torch.cuda.Event() for _ in range(n)]
+    ev_out = [torch.cuda.Event() for _ in range(n)]
+    barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s_in)
+    stream.wait_stream(s_in)
+    s_out.wait_stream(s_in)
+    for i in range(n):
+        b = i % nbuf
+        with torch.cuda.stream(s_in):
+            if i >= nbuf:
+                s_in.wait_event(ev_done[i - nbuf])  # x_dev[b] consumed by step i-nbuf
+            x_dev[b].copy_(x_host[b], non_blocking=True)
+            ev_in[i].record(s_in)
+        stream.wait_event(ev_in[i])
+        if i >= nbuf:
+            stream.wait_event(ev_out[i - nbuf])  # y_dev[b] drained by step i-nbuf's D2H
+        compute(x_dev[b], y_dev[b])
+        ev_done[i].record(stream)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(ev_done[i])
+            y_host[b].copy_(y_dev[b], non_blocking=True)
+            ev_out[i].record(s_out)
+    s_out.wait_stream(stream)
+    e1.record(s_out)
+    torch.cuda.synchronize(dev)
+    barrier()
+    return e0.elapsed_time(e1) / n
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -322,40 +364,8 @@ def run_ours(args, rank, world, local_rank):
         hbuf.copy_(x.cpu())
     x_dev = [torch.empty_like(x) for _ in range(nbuf)]
     y_dev = [torch.empty_like(y) for _ in range(nbuf)]
-    s_in = torch.cuda.Stream(dev)
-    s_out = torch.cuda.Stream(dev)
-    ev_in = [torch.cuda.Event() for _ in range(n)]
-    ev_done = [torch.cuda.Event() for _ in range(n)]
-    ev_out = [torch.cuda.Event() for _ in range(n)]
-
-    barrier()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s_in)
-    stream.wait_stream(s_in)
-    s_out.wait_stream(s_in)
-    for i in range(n):
-        b = i % nbuf
-        with torch.cuda.stream(s_in):
-            if i >= nbuf:
-                s_in.wait_event(ev_done[i - nbuf])  # x_dev[b] consumed by step i-nbuf
-            x_dev[b].copy_(x_host[b], non_blocking=True)
-            ev_in[i].record(s_in)
-        stream.wait_event(ev_in[i])
-        if i >= nbuf:
-            stream.wait_event(ev_out[i - nbuf])  # y_dev[b] drained by step i-nbuf's D2H
-        ag(x_dev[b])
-        rs(y_dev[b])
-        ev_done[i].record(stream)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_done[i])
-            y_host[b].copy_(y_dev[b], non_blocking=True)
-            ev_out[i].record(s_out)
-    s_out.wait_stream(stream)
-    e1.record(s_out)
-    torch.cuda.synchronize(dev)
-    barrier()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / n)
+    e2e_ms = max_over_ranks(e2e_pipeline(torch, n, x_host, y_host, x_dev, y_dev,
+                                          lambda xin, yout: (ag(xin), rs(yout)), stream, dev, barrier))
     e2e_value = flops_step / (e2e_ms * 1e-3) / 1e12
     h2d = x_host[0].numel() * x_host[0].element_size() * world
     d2h = y_host[0].numel() * y_host[0].element_size() * world
