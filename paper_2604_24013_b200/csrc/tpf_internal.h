@@ -73,8 +73,8 @@ struct Blame {
 constexpr int kErrWords = 8;
 
 struct KParams {
-  CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); a_mn: (rows, K, B, ranks)
-  CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); b_kmajor: (K, N, ranks)
+  CUtensorMap tmap_a;  // A operand source (x), dims (K, rows, B, hosted ranks); MN-major A: (rows, K, B, ranks)
+  CUtensorMap tmap_b;  // W, dims (N, K, hosted ranks), N contiguous (MN-major B); K-major B: (K, N, ranks)
   CUtensorMap tmap_wire[2];  // AG wire images per heap parity (128 B, 128 rows, image, slot, rank)
   int op;              // OP_RS (GEMM-RS, also the T == 1 GEMM) or OP_AG
   int mode;            // Mode (kernel instance)
@@ -89,13 +89,9 @@ struct KParams {
   int l2_a, l2_b;      // TMA L2 eviction priority of the A / B loads: 0 normal, 1 evict_first, 2 evict_last
   int ag_batch;        // AG: forwarded images per fence + flag publication (clamped to 1..8)
   int act;             // AG epilogue activation (Act)
-  int a_mn;            // A operand MN-major (rows contiguous): x stored as (K_red, rows), e.g. X for X^T dY
-  int b_kmajor;        // B operand K-major: w stored (N, K) row-major (PyTorch Linear weight layout)
-  int gather_b;        // OP_AG variant: the ring carries B (weight column blocks), not A (DP param AG)
   int64_t out_ld;      // output row stride (elements)
-  int64_t blk_cols;    // gather_b: columns of one rank's weight block (output column offset unit)
+  int64_t blk_cols;    // MODE_GATHER_B: columns of one rank's weight block (output column offset unit)
   // plain (T == 1) path extensions used by the UP attention pipeline
-  int b_batched;                      // tmap_b has a batch dim: B operand differs per batch row-block
   int heads_merge;                    // >0: batch g -> (b = g / heads, hh = g % heads), column hh*N
   int64_t a_row_off[kMaxRanks];       // per hosted rank: A row offset (query slice)
   char* out_rank[kMaxRanks];          // per hosted rank: output base (may be a peer pointer)
@@ -107,14 +103,10 @@ struct KParams {
   int nmb, nnt, nkb;   // m-blocks, n-tiles, k-blocks per step
   int npairs;          // ceil(nmb / 2): m-block pairs (one per CTA pair)
   int nsteps;          // T * m (1 when T == 1)
-  int B;
   int64_t Sc;          // rows of one sequence chunk, per batch row
-  int64_t K;           // reduction length seen by the GEMM
   int64_t N;           // output columns
   int64_t x_rows;      // x rows per batch (RS: S, AG: S/T)
   int64_t out_rows;    // out rows per batch (RS: S/T, AG: S)
-  const char* x;       // hosted rank 0's x (AG comm warps read it for hop 0)
-  int64_t x_rank_stride;
   char* out;
   int64_t out_rank_stride;
   char* sym[kMaxRanks];     // symmetric base of every rank, mapped in this process

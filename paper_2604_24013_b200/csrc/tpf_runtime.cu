@@ -347,12 +347,8 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   p.n_hosted = R;
   p.rank0 = k.rank0;
   p.act = k.act;
-  p.a_mn = k.a_mn;
-  p.b_kmajor = k.b_kmajor;
-  p.gather_b = k.gather_b;
   p.out_ld = out_ld;
   p.blk_cols = k.N;
-  p.b_batched = k.b_batched;
   p.heads_merge = k.heads_merge;
   for (int r = 0; r < tpf::kMaxRanks; ++r) {
     p.a_row_off[r] = k.a_row_off[r];
@@ -390,14 +386,10 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
   if (const char* e = std::getenv("TPF_L2_B")) p.l2_b = std::atoi(e);
   p.ag_batch = env_int("TPF_AG_BATCH", 4);
   p.nsteps = k.T * k.m;
-  p.B = static_cast<int>(k.B);
   p.Sc = k.Sc;
-  p.K = k.K;
   p.N = k.N;
   p.x_rows = k.x_rows;
   p.out_rows = k.out_rows;
-  p.x = static_cast<const char*>(k.x);
-  p.x_rank_stride = x_rank_stride;
   p.out = static_cast<char*>(k.out);
   p.out_rank_stride = k.B * k.out_rows * out_ld * esz;
   p.timeout_ns = c ? c->timeout_ns : kDefaultTimeoutNs;
