@@ -1047,6 +1047,7 @@ __global__ void __launch_bounds__(kThreads, 1) tpf_fused_kernel(const __grid_con
 template <int kOp, int kMode>
 __global__ void __launch_bounds__(kThreads, 1) tpf_fused_group_kernel(const __grid_constant__ GroupParams gp) {
   const int r = blockIdx.x / gp.p[0].ctas_per_rank;
+  if (r >= gp.n) return;  // (the grid is sized exactly; both CTAs of a pair share r)
   const KParams& p = gp.p[r];
   fused_body<kOp, kMode>(p, 0, blockIdx.x - r * p.ctas_per_rank, p.ctas_per_rank);
 }
