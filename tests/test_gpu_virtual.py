@@ -82,3 +82,38 @@ def test_virtual_dp_grad_rs_and_param_ag_exact():
         for j in range(T):
             assert torch.equal(out[:, j * Nl:(j + 1) * Nl], blk), j
     comm.close()
+
+
+def test_virtual_graph_replay_exact():
+    """AG-GEMM and GEMM-RS captured once in a CUDA graph on the virtual group and replayed: the
+    device epoch advances per replay, every wait is real, and every replay is exact."""
+    T, S, K, N = 8, 2048, 1024, 2048
+    sl, nl, kl = S // T, N // T, K // T
+    x = _ints((1, sl, K), 0, 5, 8).to(torch.bfloat16)
+    w = _ints((K, nl), -2, 2, 9).to(torch.bfloat16)
+    xr = _ints((1, S, kl), 0, 5, 10).to(torch.bfloat16)
+    wr = _ints((kl, N), -2, 2, 11).to(torch.bfloat16)
+    want_ag = (x[0].double() @ w.double()).float()
+    want_rs = (xr[0].double() @ wr.double()).view(T, sl, N).sum(0).float()
+    y = torch.zeros((1, S, nl), device=DEV)
+    yr = torch.zeros((1, sl, N), device=DEV)
+    comm = tpf.Communicator.virtual_group(T, max(tpf.sym_bytes_ag(T, 1, S, K, nl), tpf.sym_bytes_rs(T, 1, S, kl, N, 1, tpf.F32)))
+    s = torch.cuda.Stream(DEV)
+    with torch.cuda.stream(s):
+        comm.ag_gemm(x, w, y, stream=s)
+        comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.F32, stream=s)
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        comm.ag_gemm(x, w, y, stream=s)
+        comm.gemm_rs(xr, wr, yr, kind=tpf.RING, wire=tpf.F32, stream=s)
+    for _ in range(4):
+        y.zero_()
+        yr.zero_()
+        graph.replay()
+        torch.cuda.synchronize()
+        comm.sync(s)
+        for r in range(T):
+            assert torch.equal(y[0, r * sl:(r + 1) * sl], want_ag), r
+        assert torch.equal(yr[0], want_rs)
+    comm.close()
