@@ -735,7 +735,9 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
       if (kPdl && p.pdl_trigger == 2) griddep_launch_dependents();  // all of this CTA's loads issued
     } else if (warp == 1) {
       // ===================================================== MMA issuer (leader CTA)
-      if (leader && lane == 0) {
+      // The whole warp runs the loop (warp-uniform values) and elect.sync issues, so the
+      // descriptors live in uniform registers.
+      if (leader) {
         const uint32_t idesc =
             make_idesc_bf16(2 * BM, BN, /*b_mn_major=*/!kBKMajor, /*a_mn_major=*/kAMn);
         int stage = 0;
@@ -762,12 +764,12 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
               // same offsets); 16 K-rows = 2048 B; LBO = 64-col atom (64 x 128 B); SBO = 8 K-rows.
               const uint64_t bd = kBKMajor ? make_sdesc(bbase + k * 32, 0, 1024)
                                                              : make_sdesc(bbase + k * 2048, 64 * BK * 2, 1024);
-              mma_bf16_2sm(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+              mma_bf16_2sm_warp(d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
             }
-            mma_commit_2sm(empty + stage, 0x3);
+            mma_commit_2sm_warp(empty + stage, 0x3);
             if (++stage == kSt) { stage = 0; phase ^= 1; }
           }
-          mma_commit_2sm(tfull + a, 0x3);
+          mma_commit_2sm_warp(tfull + a, 0x3);
         }
       }
     } else {

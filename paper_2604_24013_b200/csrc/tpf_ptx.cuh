@@ -398,6 +398,29 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
       : "memory");
 }
 
+// Warp-wide pair MMA / commit: every lane runs the call with the same (warp-uniform) operands
+// and elect.sync picks the issuing lane inside the asm, so ptxas keeps the descriptors in
+// uniform registers (a single-lane issuer re-broadcasts them with R2UR per MMA).
+__device__ __forceinline__ void mma_bf16_2sm_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm_warp(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
 // Commit: arrive once on the barrier at this offset in every CTA of `mask`.
 __device__ __forceinline__ void mma_commit_2sm(uint64_t* bar, uint16_t mask) {
   asm volatile(
