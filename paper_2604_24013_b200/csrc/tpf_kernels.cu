@@ -601,13 +601,12 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
     if (warp == 0) {
       // ===================================================== TMA producer (both CTAs)
-      // With AG wire inputs the whole warp walks the schedule (the wire-image flag scan is
-      // warp-parallel); otherwise lane 0 alone. Lane 0 issues barrier arrivals and TMA loads.
-      const bool warp_walk = !kSingle && kOp == OP_AG && p.T > 1 && !p.compute_only;
+      // The whole warp walks the schedule (warp-uniform values; the AG wire-image flag scan is
+      // warp-parallel) and elect.sync issues the barrier arrivals and TMA loads.
       const uint64_t pol_a = l2_policy(p.l2_a), pol_b = l2_policy(p.l2_b);
       int stage = 0;
       uint32_t phase = 0;
-      for (int lin = gp; lin < ntiles && (warp_walk || lane == 0); lin += GP) {
+      for (int lin = gp; lin < ntiles; lin += GP) {
         const Tile t = get_tile(p, lin, cta);
         const int pass = t.step / p.T, it = t.step - pass * p.T;
         const bool from_wire = !kSingle && (kOp == OP_AG) && it > 0 && !p.compute_only;
@@ -631,9 +630,10 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         const uint32_t* mflags = (a_from_wire || b_from_wire) ? flag_ptr(p, par, rank, aslot, img0) : nullptr;
         int ready = -1;  // wire images [0, ready] of this operand block are known to have landed
         uint64_t t_first = 0;
-        if (kMode == MODE_QSPLIT && t.valid > 0 && lane == 0 && !p.compute_only) {
+        if (kMode == MODE_QSPLIT && t.valid > 0 && !p.compute_only) {
           // the A rows of this step's query slice come from the concurrently running attention
           // kernel (generic stores): wait for the slice's counter, then order the TMA reads
+          // (every lane acquires and fences: elect.sync picks the issuing lane)
           const int l = p.T > 1 ? p.sched[rank][it][2] : 0;
           const uint32_t* cnt = p.qs_ready[h] + l;
           if (ld_acquire_gpu(cnt) < p.qs_target) {
@@ -653,7 +653,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
           if (wire_live && kb > ready) {
             // Claim the run of consecutive landed images from kb on: every lane acquire-loads
             // one flag (image kb + lane, system scope; one round trip per poll) until image
-            // kb has landed. The warp barrier carries the acquires to lane 0, whose proxy
+            // kb has landed. The warp barrier carries the acquires to every lane, whose proxy
             // fence orders them before the TMA (async-proxy) reads. Images past the run are
             // claimed when the producer reaches them, mid-tile, behind the buffered stages.
             // (Relaxed polls plus one fence.acq_rel.sys measured 3x slower: the system fence
@@ -680,49 +680,49 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
             }
             ready = min(kb + max(run, 1) - 1, p.nkb - 1);
             __syncwarp();
-            if (lane == 0) fence_proxy_async_global();
+            fence_proxy_async_global();  // every lane: whichever lane elect.sync picks issues the TMA
             if (p.trace && lane == 0) {
               const uint64_t tw1 = globaltimer();
               if (tw1 - tw0 > 1000) trace_rec(p, TR_WAIT_A, rank, t.step, static_cast<int64_t>(lin) * 1024 + kb, tw0, tw1);
             }
           }
-          if (lane == 0) {
+          {
             mbar_wait(p, empty + stage, phase ^ 1);
             uint8_t* sa = smem_a + stage * kAStageBytes;
             uint8_t* sb = smem_b + stage * kBStageBytes;
             const uint32_t fb = mapa_shared(smem_u32(full + stage), 0);
             const int img = static_cast<int>(img0) + kb;
             if (leader)
-              mbar_arrive_expect_tx(full + stage, 2 * kStageBytes);
+              mbar_arrive_expect_tx_warp(full + stage, 2 * kStageBytes);
             else
-              mbar_arrive_cluster(fb);
+              mbar_arrive_cluster_warp(fb);
             if (a_from_wire) {
-              tma_load_2sm_5d(sa, wmap, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
+              tma_load_2sm_5d_warp(sa, wmap, fb, 0, 0, t.valid ? img : p.nmb * p.nkb, aslot, h);
             } else if (kAMn) {
               // MN-major A (e.g. X^T from row-major X): two 64-row x 64-K SW128 atoms
   #pragma unroll
               for (int q = 0; q < BM / 64; ++q)
-                tma_load_2sm_4d(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
+                tma_load_2sm_4d_warp(sa + q * (64 * BK * 2), &p.tmap_a, fb, static_cast<int>(arow) + q * 64, kb * BK,
                                 t.b, h);
             } else {
-              tma_load_2sm_4d_hint(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h, pol_a);
+              tma_load_2sm_4d_hint_warp(sa, &p.tmap_a, fb, kb * BK, static_cast<int>(arow), t.b, h, pol_a);
             }
             if (b_from_wire) {
-              tma_load_2sm_5d(sb, wmap, fb, 0, 0, img, aslot, h);
+              tma_load_2sm_5d_warp(sb, wmap, fb, 0, 0, img, aslot, h);
             } else if (kBKMajor) {
               // K-major B (w stored (N, K)): one 128-column x 64-K SW128 box
               if (kBBatched)
-                tma_load_2sm_4d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
+                tma_load_2sm_4d_warp(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), t.b, h);
               else
-                tma_load_2sm_3d(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
+                tma_load_2sm_3d_warp(sb, &p.tmap_b, fb, kb * BK, t.nt * BN + cta * (BN / 2), h);
             } else {
   #pragma unroll
               for (int q = 0; q < BN / 128; ++q) {
                 if (kBBatched)
-                  tma_load_2sm_4d(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                  tma_load_2sm_4d_warp(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                                   kb * BK, t.b, h);
                 else
-                  tma_load_2sm_3d_hint(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
+                  tma_load_2sm_3d_hint_warp(sb + q * (64 * BK * 2), &p.tmap_b, fb, t.nt * BN + cta * (BN / 2) + q * 64,
                                        kb * BK, h, pol_b);
               }
             }

@@ -398,6 +398,52 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
       : "memory");
 }
 
+// Warp-wide producer operations: every lane calls with the same (warp-uniform) operands and
+// elect.sync picks the one lane that issues, so the coordinates stay in uniform registers.
+#define TPF_ELECTED(instr) "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\telect.sync r|e, 0xffffffff;\n\t@e " instr "\n\t}"
+__device__ __forceinline__ void mbar_arrive_expect_tx_warp(uint64_t* bar, uint32_t bytes) {
+  asm volatile(TPF_ELECTED("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;") ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster_warp(uint32_t cluster_addr) {
+  asm volatile(TPF_ELECTED("mbarrier.arrive.shared::cluster.b64 _, [%0];") ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm_3d_warp(void* smem_dst, const void* tmap, uint32_t mbar, int c0, int c1,
+                                                     int c2) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                           " [%0], [%1, {%2, %3, %4}], [%5];") ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm_4d_warp(void* smem_dst, const void* tmap, uint32_t mbar, int c0, int c1,
+                                                     int c2, int c3) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                           " [%0], [%1, {%2, %3, %4, %5}], [%6];") ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm_5d_warp(void* smem_dst, const void* tmap, uint32_t mbar, int c0, int c1,
+                                                     int c2, int c3, int c4) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                           " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];") ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm_3d_hint_warp(void* smem_dst, const void* tmap, uint32_t mbar, int c0,
+                                                          int c1, int c2, uint64_t pol) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                           ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;") ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm_4d_hint_warp(void* smem_dst, const void* tmap, uint32_t mbar, int c0,
+                                                          int c1, int c2, int c3, uint64_t pol) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                           ".L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;") ::"r"(smem_u32(smem_dst)),
+               "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar), "l"(pol)
+               : "memory");
+}
+
 // Warp-wide pair MMA / commit: every lane runs the call with the same (warp-uniform) operands
 // and elect.sync picks the issuing lane inside the asm, so ptxas keeps the descriptors in
 // uniform registers (a single-lane issuer re-broadcasts them with R2UR per MMA).
