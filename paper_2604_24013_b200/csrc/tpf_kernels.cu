@@ -311,12 +311,12 @@ __device__ __noinline__ void rs_epilogue_fold_stages(const KParams& p, uint32_t 
   constexpr uint32_t kUnit = 4 * BM * 16;               // one 32-column sub-chunk of one bf16 partial
   constexpr uint32_t kBuf = (kMaxRanks - 1) * kUnit;    // one half of the double buffer
   const int nin = p.T - 1;
-  const bool issuer = ew == 0 && (threadIdx.x & 31) == 0;
+  const bool issuer = ew == 0;  // the whole warp (warp-uniform values); elect.sync issues
   auto issue = [&](int j) {
     uint8_t* dst = sbuf + (j & 1) * kBuf;
-    mbar_arrive_expect_tx(fbar + (j & 1), nin * kUnit);
+    mbar_arrive_expect_tx_warp(fbar + (j & 1), nin * kUnit);
     for (int s = 0; s < nin; ++s)
-      bulk_load(dst + s * kUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(j) * kUnit, kUnit, fbar + (j & 1));
+      bulk_load_warp(dst + s * kUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(j) * kUnit, kUnit, fbar + (j & 1));
   };
   // every warp of the group has acquired its rows' flags of all T-1 partials: the barrier carries
   // those acquires to the issuer, whose proxy fence orders them before the async-proxy copies
@@ -368,14 +368,14 @@ __device__ __noinline__ void rs_epilogue_fold_smem(const KParams& p, uint32_t ta
   constexpr uint32_t kBuf = (kMaxRanks - 1) * kFoldUnit;  // one half of the double buffer
   constexpr int kWords = BN / 8;                           // 16-B words (8 bf16 columns) per row
   const int nin = p.T - 1;
-  const bool issuer = ew == 0 && (threadIdx.x & 31) == 0;
+  const bool issuer = ew == 0;  // the whole warp (warp-uniform values); elect.sync issues
   // word u of every partial: wire_off(0, u / 4, u % 4, 0) = u * BM * 16
   auto issue = [&](int u) {
     uint8_t* dst = sbuf + (u & 1) * kBuf;
-    mbar_arrive_expect_tx(fbar + (u & 1), nin * kFoldUnit);
+    mbar_arrive_expect_tx_warp(fbar + (u & 1), nin * kFoldUnit);
     for (int s = 0; s < nin; ++s)
-      bulk_load(dst + s * kFoldUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(u) * kFoldUnit, kFoldUnit,
-                fbar + (u & 1));
+      bulk_load_warp(dst + s * kFoldUnit, in0 + s * p.slot_bytes + static_cast<int64_t>(u) * kFoldUnit, kFoldUnit,
+                     fbar + (u & 1));
   };
   // every warp of the group has acquired its rows' flags of all T-1 partials: the barrier carries
   // those acquires to the issuer, whose proxy fence orders them before the async-proxy copies

@@ -444,6 +444,12 @@ __device__ __forceinline__ void tma_load_2sm_4d_hint_warp(void* smem_dst, const 
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_load_warp(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(TPF_ELECTED("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];")
+               ::"r"(smem_u32(smem_dst)), "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
 // Warp-wide pair MMA / commit: every lane runs the call with the same (warp-uniform) operands
 // and elect.sync picks the issuing lane inside the asm, so ptxas keeps the descriptors in
 // uniform registers (a single-lane issuer re-broadcasts them with R2UR per MMA).
