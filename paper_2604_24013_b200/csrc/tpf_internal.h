@@ -48,6 +48,8 @@ enum Mode : int {
                       // a step's tiles wait for their query slice's ready counter (Alg. 4)
   MODE_RS_DIRECT = 7, // MODE_STD GEMM-RS with the pairwise schedule's rs_direct fold (its own
                       // instance: the ring / circular MODE_STD instance carries no fold code)
+  MODE_DP_DIRECT = 8, // MODE_DP_GRAD operands with the pairwise fold (the same split: the ring /
+                      // circular DP instance carries no fold code)
 };
 
 // Blame table: a waiter that gives up on a peer flag (timeout, or the group aborting) records

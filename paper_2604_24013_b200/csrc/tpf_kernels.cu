@@ -495,7 +495,7 @@ __device__ __forceinline__ void rs_epilogue_pipelined(const KParams& p, uint32_t
 // neutral on the fused AG-GEMM, so the multi-rank instances keep plain stream order.
 __host__ __device__ constexpr bool pdl_instance(int mode) {
   return mode == MODE_SINGLE || mode == MODE_STD || mode == MODE_DP_GRAD || mode == MODE_GATHER_B ||
-         mode == MODE_RS_DIRECT;
+         mode == MODE_RS_DIRECT || mode == MODE_DP_DIRECT;
 }
 
 // Operand / epilogue modes are compile-time (one instance per use): runtime flags in the
@@ -504,21 +504,22 @@ __host__ __device__ constexpr bool pdl_instance(int mode) {
 // exit_ctas = CTAs that read p's device epoch (the last of them to exit publishes it).
 template <int kOp, int kMode>
 __device__ __forceinline__ void fused_body(const KParams& p, const int h, const int g, const uint32_t exit_ctas) {
-  constexpr bool kAMn = kMode == MODE_DP_GRAD;                         // A MN-major (X^T)
+  constexpr bool kAMn = kMode == MODE_DP_GRAD || kMode == MODE_DP_DIRECT;  // A MN-major (X^T)
   constexpr bool kGatherB = kMode == MODE_GATHER_B;                    // AG carries B
   constexpr bool kBBatched = kMode == MODE_QK || kMode == MODE_PV;     // B per batch (head)
   constexpr bool kBKMajor = kGatherB || kMode == MODE_QK;              // B stored (N, K)
   constexpr bool kUpEpi = kMode == MODE_PV;                            // merge_heads + push + flags
   constexpr bool kSingle = kMode == MODE_SINGLE;                       // T == 1: no ring at all
   constexpr bool kPdl = pdl_instance(kMode);                           // launched with PDL
-  // rs_direct (pairwise) fold: its own instance for MODE_STD operands; the DP / query-split
-  // instances keep the runtime switch
-  const bool direct = kMode == MODE_RS_DIRECT || (kMode != MODE_STD && p.direct);
+  // rs_direct (pairwise) fold: its own instances for the TP and DP operands (folds staged
+  // through shared memory); the query-split / UP instances keep the runtime switch
+  constexpr bool kDirectInst = kMode == MODE_RS_DIRECT || kMode == MODE_DP_DIRECT;
+  const bool direct = kDirectInst || (kMode != MODE_STD && kMode != MODE_DP_GRAD && p.direct);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* smem_a = smem;
-  constexpr int kSt = kMode == MODE_RS_DIRECT ? kStagesDirect : kStages;  // pipeline stages
+  constexpr int kSt = kDirectInst ? kStagesDirect : kStages;  // pipeline stages
   uint8_t* smem_b = smem + kSt * kAStageBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSt * kStageBytes);
   uint64_t* full = bars;                  // leader: 2 arrivals + 2 x stage tx bytes
@@ -528,7 +529,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
   uint64_t* fold_bar = bars + 4 * kSt + 4;   // [2 groups][2 buffers]: rs_direct fold staging
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 4 * kSt + 8);
   uint64_t* fwd_bar = bars + 4 * kSt + 9;    // [2]: AG forwarder warps, their bulk / tensor loads
-  uint8_t* fold_smem = smem + kSt * kStageBytes + 2048;  // MODE_RS_DIRECT: [2 groups][kFoldGroupBytes]
+  uint8_t* fold_smem = smem + kSt * kStageBytes + 2048;  // pairwise instances: [2 groups][kFoldGroupBytes]
   uint8_t* fwd_smem = smem + kSt * kStageBytes + 1024;   // AG (both kinds): 2 x 16 KiB forwarder buffers
 
   // warp index through a shuffle so ptxas treats it (and the role branches) as warp-uniform
@@ -990,10 +991,10 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         // pairwise instance, bf16 wire: stage the fold through shared memory -- the pair's last
         // tile through its idle pipeline stages (8 KiB pieces, 32 columns at a time), every other
         // fold tile through the warpgroup's own buffers (2 KiB pieces, 8 columns at a time)
-        if (kMode == MODE_RS_DIRECT && !p.wire_f32 && tile_live && lin + GP >= ntiles)
+        if (kDirectInst && !p.wire_f32 && tile_live && lin + GP >= ntiles)
           rs_epilogue_fold_stages(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
                                   a ? tempty_leader1 : tempty_leader0, smem, fold_bar + 2 * eg, eg, ew);
-        else if (kMode == MODE_RS_DIRECT && !p.wire_f32 && tile_live)
+        else if (kDirectInst && !p.wire_f32 && tile_live)
           rs_epilogue_fold_smem(p, taddr, in0, rp, static_cast<int64_t>(t.nt) * BN, row, valid,
                                 a ? tempty_leader1 : tempty_leader0, fold_smem + eg * kFoldGroupBytes,
                                 fold_bar + 2 * eg, eg, ew);
@@ -1101,7 +1102,7 @@ cudaError_t launch_instance(const Params& p, int grid, cudaStream_t stream) {
     kern = tpf_fused_kernel<kOp, kMode>;
   static uint64_t attr_done = 0;
   static bool pool_ok[64];
-  constexpr int kSmem = kMode == MODE_RS_DIRECT                        ? kSmemBytesDirect
+  constexpr int kSmem = (kMode == MODE_RS_DIRECT || kMode == MODE_DP_DIRECT) ? kSmemBytesDirect
                         : (kOp == OP_AG && (kMode == MODE_STD || kMode == MODE_GATHER_B)) ? kSmemBytesFwd
                                                               : kSmemBytes;
   once_per_device(attr_done, [kern] {
@@ -1156,6 +1157,7 @@ cudaError_t launch_fused(const KParams& p, int grid, cudaStream_t stream) {
     case MODE_PV: return launch_instance<OP_RS, MODE_PV>(p, grid, stream);
     case MODE_QSPLIT: return launch_instance<OP_RS, MODE_QSPLIT>(p, grid, stream);
     case MODE_RS_DIRECT: return launch_instance<OP_RS, MODE_RS_DIRECT>(p, grid, stream);
+    case MODE_DP_DIRECT: return launch_instance<OP_RS, MODE_DP_DIRECT>(p, grid, stream);
     case MODE_SINGLE:
       return p.op == OP_AG ? launch_instance<OP_AG, MODE_SINGLE>(p, grid, stream)
                            : launch_instance<OP_RS, MODE_SINGLE>(p, grid, stream);
@@ -1173,6 +1175,7 @@ cudaError_t launch_fused_group(const GroupParams& gp, int grid, cudaStream_t str
     case MODE_DP_GRAD: return launch_instance<OP_RS, MODE_DP_GRAD>(gp, grid, stream);
     case MODE_GATHER_B: return launch_instance<OP_AG, MODE_GATHER_B>(gp, grid, stream);
     case MODE_RS_DIRECT: return launch_instance<OP_RS, MODE_RS_DIRECT>(gp, grid, stream);
+    case MODE_DP_DIRECT: return launch_instance<OP_RS, MODE_DP_DIRECT>(gp, grid, stream);
     default: return cudaErrorInvalidValue;  // other instances are not split-group operations
   }
 }

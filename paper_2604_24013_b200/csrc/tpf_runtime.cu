@@ -339,6 +339,7 @@ tpf::Status launch(tpf_comm* c, const Call& k, cudaStream_t stream) {
          : k.T == 1 ? tpf::MODE_SINGLE
          : tpf::MODE_STD;
   if (p.mode == tpf::MODE_STD && k.op == tpf::OP_RS && k.direct) p.mode = tpf::MODE_RS_DIRECT;
+  if (p.mode == tpf::MODE_DP_GRAD && k.direct) p.mode = tpf::MODE_DP_DIRECT;
   if ((p.mode == tpf::MODE_STD || p.mode == tpf::MODE_SINGLE) && k.b_kmajor)
     return tpf::Status::invalid("internal: K-major B is only instantiated for the DP / UP modes");
   p.T = k.T;

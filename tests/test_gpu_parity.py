@@ -459,17 +459,43 @@ def test_dp_grad_rs_exact(T):
     comm.close()
 
 
-def test_dp_grad_rs_full_size_replay():
+@pytest.mark.parametrize("T", [2, 4, 8])
+def test_dp_grad_rs_pairwise_bf16_wire_exact(T):
+    """Pairwise DP gradient RS over the bf16 wire (its own kernel instance, folds staged
+    through shared memory): exact on small-integer data whose partials bf16 holds exactly."""
+    M, K, N = 96, 64 * T, 520
+    X = np.stack([O.randint((M, K), 0, 2, 160 + r) for r in range(T)])
+    dY = np.stack([O.randint((M, N), -1, 2, 170 + r) for r in range(T)])
+    parts = np.stack([(X[r].T @ dY[r])[None] for r in range(T)])
+    assert np.abs(parts).max() <= 256
+    Xd = torch.stack([bf16(X[r]) for r in range(T)]).to(DEV)
+    dYd = torch.stack([bf16(dY[r]) for r in range(T)]).to(DEV)
+    comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, 1, K, M, N, 1, tpf.BF16))
+    for out_dtype in (torch.float32, torch.bfloat16):
+        dW = torch.full((T, K // T, N), float("nan"), device=DEV, dtype=out_dtype)
+        comm.dp_grad_rs(Xd, dYd, dW, kind=tpf.PAIRWISE, wire=tpf.BF16)
+        comm.sync()
+        want = torch.from_numpy(O.fuse_rs_identity(T, tpf.PAIRWISE, 1, parts)[:, 0])
+        want = want.to(out_dtype).double()  # the exact fp32 sum rounded once on output
+        assert torch.equal(dW.double().cpu(), want), out_dtype
+    comm.close()
+
+
+@pytest.mark.parametrize("kind", [tpf.RING, tpf.PAIRWISE])
+def test_dp_grad_rs_full_size_replay(kind):
     """cfg 4 shapes (a Llama-3.2-1B-class MLP weight, 8 DP ranks, 4096 tokens/rank):
-    bf16 wire ring RS of dW is bit-exact vs an fp32 replay of the ring order over the
-    library's own single-rank partials."""
+    the bf16-wire RS of dW is bit-exact vs an fp32 replay of the schedule's reduction order
+    over the library's own single-rank partials (ring: the running sum rounded to bf16 at
+    each hop; pairwise: the T-1 received partials rounded to bf16, folded in schedule order,
+    then the own partial). In the 8-rank local group each rank has 9 CTA pairs for 32
+    last-step tiles, so the pairwise fold runs both staged paths."""
     T, M, K, N = 8, 4096, 2048, 8192
     g = torch.Generator(device=DEV).manual_seed(3)
     X = torch.randn((T, M, K), device=DEV, generator=g).to(torch.bfloat16)
     dY = (torch.randn((T, M, N), device=DEV, generator=g) / 64).to(torch.bfloat16)
     dW = torch.empty((T, K // T, N), device=DEV)
     comm = tpf.Communicator.local_group(T, tpf.sym_bytes_rs(T, 1, K, M, N, 1, tpf.BF16))
-    comm.dp_grad_rs(X, dY, dW, kind=tpf.RING, wire=tpf.BF16)
+    comm.dp_grad_rs(X, dY, dW, kind=kind, wire=tpf.BF16)
     comm.sync()
     comm.close()
     one = tpf.Communicator.create(0, 1, 0)
@@ -480,13 +506,21 @@ def test_dp_grad_rs_full_size_replay():
         full.append(o)
     one.sync()
     one.close()
-    sched = tpf.build_schedule(tpf.RING, T)
+    sched = tpf.build_schedule(kind, T)
     kl = K // T
     for r in (0, 5):
-        chain = [next(q for q in range(T) if sched[q][i][2] == r) for i in range(T)]
-        acc = full[chain[0]][r * kl:(r + 1) * kl]
-        for q in chain[1:]:
-            acc = full[q][r * kl:(r + 1) * kl] + acc.to(torch.bfloat16).float()
+        part = lambda q: full[q][r * kl:(r + 1) * kl]
+        if kind == tpf.PAIRWISE:
+            order = [sched[r][i][1] for i in range(T - 1)]
+            acc = part(order[0]).to(torch.bfloat16).float()
+            for q in order[1:]:
+                acc = acc + part(q).to(torch.bfloat16).float()
+            acc = acc + part(r)
+        else:
+            chain = [next(q for q in range(T) if sched[q][i][2] == r) for i in range(T)]
+            acc = part(chain[0])
+            for q in chain[1:]:
+                acc = part(q) + acc.to(torch.bfloat16).float()
         assert torch.equal(dW[r], acc), r
 
 

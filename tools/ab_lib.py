@@ -2,7 +2,8 @@
 cfg3 shapes, AG-GEMM and GEMM-RS), alternating processes to cancel power-cap drift. Prints
 the median us per call (20 back-to-back calls) for each build.
     python tools/ab_lib.py LIB_A LIB_B [rounds]
-A spec may carry environment settings: 'lib.so@TPF_AG_SPLIT=0@TPF_X=1'."""
+A spec may carry environment settings: 'lib.so@TPF_AG_SPLIT=0@TPF_X=1'. AB_ONLY=cfg4 runs only
+the cfg4 DP rows."""
 import json
 import os
 import statistics
@@ -24,7 +25,8 @@ def loop(fn, n=20):
     return 1e3 * e0.elapsed_time(e1) / n
 res = {}
 T = int(os.environ.get("AB_T", "8"))
-for cfg, S, K_ag, N_ag, K_rs, N_rs in (("cfg2", 8192, 4096, 28672, 14336, 4096), ("cfg3", 16384, 8192, 10240, 8192, 8192)):
+CFGS = (("cfg2", 8192, 4096, 28672, 14336, 4096), ("cfg3", 16384, 8192, 10240, 8192, 8192))
+for cfg, S, K_ag, N_ag, K_rs, N_rs in (() if os.environ.get("AB_ONLY") == "cfg4" else CFGS):
     g = torch.Generator(device=dev).manual_seed(0)
     x = torch.randn((1, S // T, K_ag), device=dev, generator=g).to(torch.bfloat16)
     w = (torch.randn((K_ag, N_ag // T), device=dev, generator=g) / 64).to(torch.bfloat16)
@@ -59,6 +61,7 @@ if T == 8:
                                                  tpf.sym_bytes_dp_ag(T, K, N // T)))
     res["cfg4_param_ag"] = loop(lambda: comm.dp_param_ag_gemm(X, Wr, out))
     res["cfg4_grad_rs"] = loop(lambda: comm.dp_grad_rs(X, dY, dW, kind=tpf.RING, wire=tpf.BF16))
+    res["cfg4_grad_rs_pw"] = loop(lambda: comm.dp_grad_rs(X, dY, dW, kind=tpf.PAIRWISE, wire=tpf.BF16))
     comm.close()
 print(json.dumps(res))
 '''
