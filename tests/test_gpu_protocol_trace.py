@@ -52,18 +52,23 @@ def test_rs_sends_in_exactly_t_minus_1_iterations_and_not_in_the_last(T):
             # NoCommunicationPostedInFinalIteration + exactly T - 1 sending iterations
             assert sorted({q.step for q in flags}) == list(range(T - 1)), (kind, r)
             assert sorted({q.step for q in tiles}) == list(range(T)), (kind, r)
-            # OwnSliceComputedLast: the schedule's final iteration is the own slice, and on the
-            # timeline the last tile to finish belongs to the final iteration. Pairwise: the
-            # final fold waits on the partners' step T-2 partials, not on this rank's own step
-            # T-2 tiles, which run in the same round on other CTA pairs and may end a little
-            # later; a pipelined step T-1 tile waits on the predecessor's step T-2 chain.
+            # OwnSliceComputedLast: the schedule's final iteration is the own slice (an
+            # iteration-order property in the reference). On the timeline, each final-step tile
+            # ends after every transfer it consumes was posted: the predecessor's step T-2
+            # running sum (pipelined) or all T-1 partners' partials (pairwise). (Not after this
+            # rank's own step T-2 tiles: those feed another rank and run in the same round on
+            # other CTA pairs, so they may end slightly later.)
             assert sched[r][T - 1] == (-1, -1, r)
-            last_step = max(tiles, key=lambda q: q.t1).step
-            if kind == tpf.PAIRWISE:
-                assert last_step >= T - 2, (kind, r)
-                assert max(q.t1 for q in tiles if q.step == T - 1) >= max(q.t0 for q in tiles), (kind, r)
-            else:
-                assert last_step == T - 1, (kind, r)
+            per_step = len({q.index for q in tiles if q.step == 0})  # (several records per tile)
+            assert {q.index for q in tiles} == set(range(T * per_step)), (kind, r)
+            consumed = range(T - 1) if kind == tpf.PAIRWISE else [T - 2]
+            for tile in range(per_step):
+                end = max(q.t1 for q in tiles if q.step == T - 1 and q.index % per_step == tile)
+                for s in consumed:
+                    src = sched[r][s][1]
+                    posted = [q.t1 for q in recs if q.rank == src and q.kind == trace.TR_FLAG and q.step == s
+                              and q.index % per_step == tile]
+                    assert posted and max(posted) <= end, (kind, r, tile, s, src)
             # every transfer is published before the rank's last tile ends (no tail)
             assert max(q.t1 for q in flags) <= max(q.t1 for q in tiles), (kind, r)
     comm.close()
