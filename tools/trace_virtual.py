@@ -78,7 +78,8 @@ def show(name, fn, compute_only=False):
     tk = min(r.t0 for r in recs if r.t0 > 0)
     for r in ml:
         st = steps.setdefault(r.step, [1e18, 0, 0])
-        st[0] = min(st[0], r.t0)
+        if r.t0 > 0:  # (a record whose start was not stamped carries t0 = 0)
+            st[0] = min(st[0], r.t0)
         st[1] = max(st[1], r.t1)
     for r in ep:
         steps.setdefault(r.step, [1e18, 0, 0])[2] = max(steps[r.step][2], r.t1)
