@@ -78,13 +78,11 @@ def show(name, fn, compute_only=False):
     tk = min(r.t0 for r in recs if r.t0 > 0)
     for r in ml:
         st = steps.setdefault(r.step, [1e18, 0, 0])
-        if r.t0 > 0:  # (a record whose start was not stamped carries t0 = 0)
-            st[0] = min(st[0], r.t0)
         st[1] = max(st[1], r.t1)
     for r in ep:
         steps.setdefault(r.step, [1e18, 0, 0])[2] = max(steps[r.step][2], r.t1)
-    print("    steps (mainloop first start / last end / last epilogue end, us): " +
-          " ".join(f"{k}:{(v[0] - tk) / 1e3:.0f}/{(v[1] - tk) / 1e3:.0f}/{(v[2] - tk) / 1e3:.0f}"
+    print("    steps (mainloop last end / last epilogue end, us): " +
+          " ".join(f"{k}:{(v[1] - tk) / 1e3:.0f}/{(v[2] - tk) / 1e3:.0f}"
                    for k, v in sorted(steps.items())), flush=True)
     for kind in (trace.TR_EPI_LOOP, trace.TR_PUBLISH, trace.TR_FLUSH, trace.TR_WAIT_IN, trace.TR_WAIT_A):
         rr = [r for r in recs if r.kind == kind]
