@@ -55,9 +55,9 @@ if have(f"{G}/{P}_bench_k.ncu-rep"):
     hdr = ("# bench.py --emulate-tp 0, launches 7-8 (after warm-up): AG-GEMM gate||up + fused SwiGLU "
            "(tpf_fused_kernel<1,5>) and GEMM-RS down\n# (<0,5>), T = 1. ncu --set full --clock-control none "
            f"(isolated, cold cache): AG 1.924 TFLOP / {d[0]:.4f} ms = {1.924145 / d[0] * 1e3:.0f} TF/s;\n"
-           f"# RS 0.962 TFLOP / {d[1]:.4f} ms = {0.962072 / d[1] * 1e3:.0f} TF/s. Tensor-pipe note: every MMA is\n"
-           "# cta_group::2 and only the issuing SM counts sm__pipe_tensor_cycles_active (DESIGN 4c); use\n"
-           "# sm__mem_tensor_cycles_active or the FLOP rate.\n")
+           f"# RS 0.962 TFLOP / {d[1]:.4f} ms = {0.962072 / d[1] * 1e3:.0f} TF/s. Tensor-pipe note: for these\n"
+           "# cta_group::2 kernels sm__pipe_tensor_cycles_active does not track the FLOP rate (DESIGN 4c);\n"
+           "# use sm__mem_tensor_cycles_active or the FLOP rate.\n")
     open(os.path.join(PR, f"{P}_fused_kernels_ncu_full.txt"), "w").write(hdr + out)
     tr_path = os.path.join(PR, "traffic.json")
     tr = json.load(open(tr_path))
