@@ -1011,7 +1011,7 @@ __device__ __forceinline__ void fused_body(const KParams& p, const int h, const 
         if (p.wire_f32)
           rs_epilogue_pipelined<true, 1>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid, last, tempty_a);
         else
-          rs_epilogue_pipelined<false, kMode == MODE_STD ? 4 : 2>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid,
+          rs_epilogue_pipelined<false, (kMode == MODE_STD || kMode == MODE_DP_GRAD) ? 4 : 2>(p, taddr, inbox, dst_tile, rp, ocol0, row, valid,
                                                                  last, tempty_a);
       }
       if (p.trace && lane == 0 && ew == 0 && tile_live)
