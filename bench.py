@@ -302,8 +302,11 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank) if rank == 0 else None
     if sampler:
         sampler.wait_ready()
-        for _ in range(max(3, args.warmup)):  # keep the GPU busy while sampling settles
-            ag(); rs()
+    barrier()
+    # keep the GPU busy while sampling settles; every rank runs these (the fused ops are
+    # collective: a call only rank 0 made would wait on peers that never join it)
+    for _ in range(max(3, args.warmup)):
+        ag(); rs()
     n = args.steps
     ev = _events(n)
     barrier()

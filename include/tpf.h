@@ -116,6 +116,9 @@ int tpf_comm_create_split_group(int world, size_t sym_bytes, tpf_comm** comms);
 int tpf_comm_destroy(tpf_comm* c);
 int tpf_comm_rank(const tpf_comm* c);
 int tpf_comm_world(const tpf_comm* c);
+/* CUDA device the communicator was created on (the library's current device at creation;
+ * every call must run with that device current), -1 for a null handle */
+int tpf_comm_device(const tpf_comm* c);
 /* The rank that failed, as GroupError::failing_rank() (fabric.hpp:22-31): set by the last
  * tpf_comm_sync that returned TPF_E_PEER (-1 before). Waiters that give up record the rank
  * they were blocked on in every rank's blame table; sync follows that chain from the rank

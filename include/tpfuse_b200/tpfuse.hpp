@@ -287,6 +287,15 @@ class RankEndpoint {
  public:
   RankEndpoint(int rank, int world, size_t sym_bytes) {
     detail::check(tpf_comm_create(rank, world, sym_bytes, &c_));
+    // The library links its own CUDA runtime: it must see the device this process made current.
+    int dev = -1;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev != tpf_comm_device(c_)) {
+      const int lib_dev = tpf_comm_device(c_);
+      tpf_comm_destroy(c_);
+      c_ = nullptr;
+      throw std::runtime_error("tpfuse: communicator created on device " + std::to_string(lib_dev) +
+                               " but the current device is " + std::to_string(dev));
+    }
   }
   ~RankEndpoint() {
     if (c_) tpf_comm_destroy(c_);

@@ -83,6 +83,7 @@ _lib.tpf_comm_failing_rank.argtypes = [_vp]
 _lib.tpf_comm_ipc_handle.argtypes = [_vp, _vp]
 _lib.tpf_comm_open_peers.argtypes = [_vp, _vp]
 _lib.tpf_comm_destroy.argtypes = [_vp]
+_lib.tpf_comm_device.argtypes = [_vp]
 _lib.tpf_comm_sync.argtypes = [_vp, _vp]
 _lib.tpf_comm_set_timeout_ns.argtypes = [_vp, _i64]
 _lib.tpf_comm_inject_fault.argtypes = [_vp, C.c_int]
@@ -124,6 +125,7 @@ EXPORTED_SYMBOLS = (
     "tpf_comm_destroy",
     "tpf_comm_rank",
     "tpf_comm_world",
+    "tpf_comm_device",
     "tpf_comm_sync",
     "tpf_comm_set_timeout_ns",
     "tpf_comm_inject_fault",
@@ -238,6 +240,13 @@ class Communicator:
             import torch
             device = torch.device("cuda", torch.cuda.current_device())
         self.device = device
+        # The library links its own (static) CUDA runtime. It must see the device torch made
+        # current, or its kernels would run on another GPU than the tensors they are given.
+        lib_dev = _lib.tpf_comm_device(self._h)
+        if lib_dev != device.index:
+            _lib.tpf_comm_destroy(self._h)
+            raise TpfCudaError(f"communicator created on device {lib_dev}, but the tensors' device is "
+                               f"cuda:{device.index} (call torch.cuda.set_device first)")
 
     def _lead(self):
         # local groups take rank-stacked tensors: a leading dim of `world`

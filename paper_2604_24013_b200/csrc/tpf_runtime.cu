@@ -730,6 +730,8 @@ int tpf_comm_rank(const tpf_comm* c) { return c ? c->rank : -1; }
 int tpf_comm_failing_rank(const tpf_comm* c) { return c ? c->failing_rank : -1; }
 int tpf_comm_world(const tpf_comm* c) { return c ? c->world : -1; }
 
+int tpf_comm_device(const tpf_comm* c) { return c ? c->device : -1; }
+
 int tpf_comm_set_timeout_ns(tpf_comm* c, int64_t ns) {
   if (!c) return fail(tpf::Status::invalid("null communicator"));
   c->timeout_ns = ns > 0 ? ns : env_timeout_ns();
