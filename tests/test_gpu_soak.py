@@ -19,8 +19,10 @@ def test_mixed_operator_sequence_on_one_communicator():
     B, S, D, H = 1, 128 * T, 256, 128 * T
     heads, Dh = 4, 128
     rng = np.random.default_rng(2027)
+    Md = 96  # DP tokens per rank
     need = max(tpf.sym_bytes_ag(T, B, S, D, H // T), tpf.sym_bytes_rs(T, B, S, H // T, D, 2),
-               tpf.sym_bytes_ulysses(T, B, heads * T, S, Dh), tpf.sym_bytes_dp_ag(T, D, H // T))
+               tpf.sym_bytes_ulysses(T, B, heads * T, S, Dh), tpf.sym_bytes_dp_ag(T, D, H // T),
+               tpf.sym_bytes_rs(T, 1, D, Md, H, 1, tpf.BF16))
     comm = tpf.Communicator.local_group(T, need)
     ref = tpf.Communicator.local_group(T, need)  # a second group computes eager references
     s = torch.cuda.Stream(DEV)
@@ -72,8 +74,34 @@ def test_mixed_operator_sequence_on_one_communicator():
         c.ulysses_attention(*sq, out_ul, B, heads * T, stream=s)
         return lambda: torch.equal(out_ul, want_ul)
 
-    ops = [lambda c: run_ag(c), lambda c: run_a2a(c), lambda c: run_ul(c)]
+    # DP ops (cfg 4 family): the gradient RS through both of its kernel instances (ring, and the
+    # pairwise one over the bf16 wire: small-integer partials bf16 holds exactly) and the
+    # parameter AG fused into the forward GEMM
+    Xg = O.randint((T, Md, D), 0, 2, 7)
+    dYg = O.randint((T, Md, H), -1, 2, 8)
+    parts = np.stack([(Xg[r].T @ dYg[r])[None] for r in range(T)])
+    dp_kinds = [tpf.RING] + ([tpf.PAIRWISE] if T % 2 == 0 else [])
+    wants_dp = {k: O.fuse_rs_identity(T, k, 1, parts)[:, 0] for k in dp_kinds}
+    Xg_d = torch.stack([bf16(Xg[r]) for r in range(T)]).to(DEV)
+    dYg_d = torch.stack([bf16(dYg[r]) for r in range(T)]).to(DEV)
+    out_dp = torch.empty((T, D // T, H), device=DEV)
+
+    def run_dp(c, k):
+        c.dp_grad_rs(Xg_d, dYg_d, out_dp, kind=k, wire=tpf.BF16, stream=s)
+        return lambda: np.array_equal(out_dp.double().cpu().numpy(), wants_dp[k])
+
+    Wp = O.randint((H, D), -2, 2, 9)  # (N = Nl * T, K), row-sharded (PyTorch Linear layout)
+    Wp_d = torch.stack([bf16(Wp[r * (H // T):(r + 1) * (H // T)]) for r in range(T)]).to(DEV)
+    want_pa = np.stack([Xg[r] @ Wp.T for r in range(T)])
+    out_pa = torch.empty((T, Md, H), device=DEV)
+
+    def run_pa(c):
+        c.dp_param_ag_gemm(Xg_d, Wp_d, out_pa, stream=s)
+        return lambda: np.array_equal(out_pa.double().cpu().numpy(), want_pa)
+
+    ops = [lambda c: run_ag(c), lambda c: run_a2a(c), lambda c: run_ul(c), lambda c: run_pa(c)]
     ops += [(lambda k, m: (lambda c: run_rs(c, k, m)))(k, m) for (k, m) in wants_rs]
+    ops += [(lambda k: (lambda c: run_dp(c, k)))(k) for k in dp_kinds]
 
     # a captured graph of two different collectives, replayed in the middle of the sequence
     with torch.cuda.stream(s):
