@@ -194,7 +194,7 @@ def _timed_calls(fn, stream, n):
 def traced_tail(comm, fn, dev):
     """Measured no_tail_check (costmodel.cpp:163-176 on a %globaltimer timeline):
     one traced call; per rank, the last peer-flag publication minus the end of the last GEMM
-    tile. Returns (max tail us over this process's ranks, steps seen)."""
+    tile. Returns the max tail in us over this process's ranks."""
     import torch
 
     from paper_2604_24013_b200 import trace
